@@ -1,0 +1,288 @@
+// engine.cu -- context, device-resident ratings, work plans, sharding.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "engine.h"
+
+namespace ab2 {
+
+// ------------------------------------------------------------------ Ctx --
+Ctx::Ctx(int dev) : device(dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw Error(ALSNCG_ECUDA, "no CUDA device visible (the product path has no CPU fallback)");
+  if (dev < 0 || dev >= n) throw Error(ALSNCG_EINVAL, "device index out of range");
+  AB2_CUDA(cudaSetDevice(dev));
+  AB2_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+  AB2_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  AB2_CUDA(cudaMalloc(&d_red, sizeof(double) * 2 * 8 * 4 * 148));
+  AB2_CUDA(cudaMalloc(&d_counters, sizeof(unsigned) * 64));
+  AB2_CUDA(cudaMemset(d_counters, 0, sizeof(unsigned) * 64));
+  AB2_CUDA(cudaMalloc(&d_scalars, sizeof(double) * 64));
+  AB2_CUDA(cudaMemset(d_scalars, 0, sizeof(double) * 64));
+  AB2_CUDA(cudaMallocHost(&h_scalars, sizeof(double) * 64));
+}
+
+Ctx::~Ctx() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& p : pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  for (void* p : scratch_ptr)
+    if (p) cudaFree(p);
+  cudaFree(d_red);
+  cudaFree(d_counters);
+  cudaFree(d_scalars);
+  cudaFreeHost(h_scalars);
+  if (comm) ncclCommDestroy(comm);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void* Ctx::scratch(int slot, size_t bytes) {
+  if (slot >= static_cast<int>(scratch_ptr.size())) {
+    scratch_ptr.resize(slot + 1, nullptr);
+    scratch_size.resize(slot + 1, 0);
+  }
+  if (scratch_size[slot] < bytes) {
+    if (scratch_ptr[slot]) {
+      AB2_CUDA(cudaStreamSynchronize(stream));
+      AB2_CUDA(cudaFree(scratch_ptr[slot]));
+      scratch_ptr[slot] = nullptr;
+    }
+    const size_t want = std::max(bytes, scratch_size[slot] + scratch_size[slot] / 2);
+    AB2_CUDA(cudaMalloc(&scratch_ptr[slot], want));
+    scratch_size[slot] = want;
+  }
+  return scratch_ptr[slot];
+}
+
+int Ctx::begin_launch(const char* name) {
+  ++launches;
+  if (!profiling) return -1;
+  int k = 0;
+  for (; k < static_cast<int>(stats.size()); ++k)
+    if (stats[k].name == name) break;
+  if (k == static_cast<int>(stats.size())) stats.push_back({name, 0, 0.0});
+  Pending p;
+  p.stat = k;
+  auto take = [&]() {
+    cudaEvent_t e;
+    if (!event_pool.empty()) {
+      e = event_pool.back();
+      event_pool.pop_back();
+    } else {
+      AB2_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  };
+  p.a = take();
+  p.b = take();
+  AB2_CUDA(cudaEventRecord(p.a, stream));
+  pending.push_back(p);
+  return static_cast<int>(pending.size()) - 1;
+}
+
+void Ctx::end_launch(int token) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(ALSNCG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  if (token >= 0) AB2_CUDA(cudaEventRecord(pending[token].b, stream));
+}
+
+void Ctx::collect_stats() {
+  AB2_CUDA(cudaStreamSynchronize(stream));
+  for (auto& p : pending) {
+    float ms = 0.f;
+    AB2_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    stats[p.stat].launches += 1;
+    stats[p.stat].ms += ms;
+    event_pool.push_back(p.a);
+    event_pool.push_back(p.b);
+  }
+  pending.clear();
+}
+
+void Ctx::sync() { AB2_CUDA(cudaStreamSynchronize(stream)); }
+
+void Ctx::fetch_scalars(int n) {
+  AB2_CUDA(cudaMemcpyAsync(h_scalars, d_scalars, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+  AB2_CUDA(cudaStreamSynchronize(stream));
+}
+
+// ------------------------------------------------------------ sharding --
+std::vector<int> partition_rows(int n_rows, const int64_t* ptr, int world, int align) {
+  std::vector<int> b(world + 1, 0);
+  b[world] = n_rows;
+  const int64_t total = ptr[n_rows];
+  for (int r = 1; r < world; ++r) {
+    const int64_t target = total * r / world;
+    int row = static_cast<int>(std::lower_bound(ptr, ptr + n_rows + 1, target) - ptr);
+    row = std::min(n_rows, ((row + align / 2) / align) * align);
+    b[r] = std::max(b[r - 1], row);
+  }
+  return b;
+}
+
+void allgather_rows(Ctx* ctx, double* rows, const std::vector<int>& bounds, int ld) {
+  if (ctx->world <= 1) return;
+  AB2_NCCL(ncclGroupStart());
+  for (int r = 0; r < ctx->world; ++r) {
+    const size_t count = static_cast<size_t>(bounds[r + 1] - bounds[r]) * ld;
+    if (count == 0) continue;
+    double* p = rows + static_cast<size_t>(bounds[r]) * ld;
+    AB2_NCCL(ncclBroadcast(p, p, count, ncclDouble, r, ctx->comm, ctx->stream));
+  }
+  AB2_NCCL(ncclGroupEnd());
+}
+
+// -------------------------------------------------------------- upload --
+namespace {
+
+void upload_view(Ctx* ctx, View& v, int row0, int row1, const int64_t* ptr, const int* idx,
+                 const double* val) {
+  v.row0 = row0;
+  v.nrows = row1 - row0;
+  const int64_t base = ptr[row0];
+  v.nnz = ptr[row1] - base;
+  v.h_ptr.resize(v.nrows + 1);
+  for (int r = 0; r <= v.nrows; ++r) v.h_ptr[r] = ptr[row0 + r] - base;
+  AB2_CUDA(cudaMalloc(&v.ptr, sizeof(int64_t) * (v.nrows + 1)));
+  AB2_CUDA(cudaMalloc(&v.idx, sizeof(int) * std::max<int64_t>(v.nnz, 1)));
+  AB2_CUDA(cudaMalloc(&v.val, sizeof(double) * std::max<int64_t>(v.nnz, 1)));
+  AB2_CUDA(cudaMemcpyAsync(v.ptr, v.h_ptr.data(), sizeof(int64_t) * (v.nrows + 1),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  if (v.nnz > 0) {
+    AB2_CUDA(cudaMemcpyAsync(v.idx, idx + base, sizeof(int) * v.nnz, cudaMemcpyHostToDevice, ctx->stream));
+    AB2_CUDA(cudaMemcpyAsync(v.val, val + base, sizeof(double) * v.nnz, cudaMemcpyHostToDevice, ctx->stream));
+  }
+}
+
+void free_view(View& v) {
+  cudaFree(v.ptr);
+  cudaFree(v.idx);
+  cudaFree(v.val);
+  v.ptr = nullptr;
+  v.idx = nullptr;
+  v.val = nullptr;
+}
+
+}  // namespace
+
+DevRatings* upload_ratings(Ctx* ctx, int n_u, int n_m, int64_t nnz, const int64_t* uptr,
+                           const int* uidx, const double* uval, const int64_t* iptr,
+                           const int* iidx, const double* ival) {
+  if (n_u < 0 || n_m < 0 || nnz < 0) throw Error(ALSNCG_EINVAL, "negative ratings dimensions");
+  if (uptr[0] != 0 || uptr[n_u] != nnz || iptr[0] != 0 || iptr[n_m] != nnz)
+    throw Error(ALSNCG_EDATA, "CSR/CSC pointers do not span nnz");
+  AB2_CUDA(cudaSetDevice(ctx->device));
+  auto R = std::make_unique<DevRatings>();
+  R->ctx = ctx;
+  R->n_u = n_u;
+  R->n_m = n_m;
+  R->nnz = nnz;
+  R->ub = partition_rows(n_u, uptr, ctx->world, kTileRows);
+  R->mb = partition_rows(n_m, iptr, ctx->world, kTileRows);
+  upload_view(ctx, R->users, R->ub[ctx->rank], R->ub[ctx->rank + 1], uptr, uidx, uval);
+  upload_view(ctx, R->items, R->mb[ctx->rank], R->mb[ctx->rank + 1], iptr, iidx, ival);
+  ctx->sync();
+  return R.release();
+}
+
+DevRatings::~DevRatings() {
+  if (ctx) cudaSetDevice(ctx->device);
+  free_view(users);
+  free_view(items);
+  for (auto& m : plans)
+    for (auto& kv : m) cudaFree(kv.second->block);
+}
+
+const SegPlan& DevRatings::plan(int kind, int S) {
+  auto& m = plans[kind];
+  auto it = m.find(S);
+  if (it != m.end()) return *it->second;
+  const View& v = view(kind);
+  auto P = std::make_unique<SegPlan>();
+  P->S = S;
+  std::vector<int> row, len, slot;
+  std::vector<int64_t> beg;
+  std::vector<int> mrow, mslot0, mnslot;
+  // heavy rows first (their segments), then single-segment rows by
+  // descending count: big work items are scheduled first.
+  std::vector<int> singles;
+  int n_slots = 0;
+  for (int r = 0; r < v.nrows; ++r) {
+    const int64_t c = v.h_ptr[r + 1] - v.h_ptr[r];
+    if (c > S) {
+      const int ns = static_cast<int>((c + S - 1) / S);
+      mrow.push_back(r);
+      mslot0.push_back(n_slots);
+      mnslot.push_back(ns);
+      for (int s = 0; s < ns; ++s) {
+        row.push_back(r);
+        beg.push_back(v.h_ptr[r] + static_cast<int64_t>(s) * S);
+        len.push_back(static_cast<int>(std::min<int64_t>(S, c - static_cast<int64_t>(s) * S)));
+        slot.push_back(n_slots + s);
+      }
+      n_slots += ns;
+    } else {
+      singles.push_back(r);
+    }
+  }
+  std::stable_sort(singles.begin(), singles.end(), [&](int a, int b) {
+    return v.h_ptr[a + 1] - v.h_ptr[a] > v.h_ptr[b + 1] - v.h_ptr[b];
+  });
+  for (int r : singles) {
+    row.push_back(r);
+    beg.push_back(v.h_ptr[r]);
+    len.push_back(static_cast<int>(v.h_ptr[r + 1] - v.h_ptr[r]));
+    slot.push_back(-1);
+  }
+  P->n_seg = static_cast<int>(row.size());
+  P->n_multi = static_cast<int>(mrow.size());
+  P->n_slots = n_slots;
+  const size_t ns = std::max<size_t>(row.size(), 1), nm = std::max<size_t>(mrow.size(), 1);
+  const size_t bytes = ns * (8 + 4 + 4 + 4) + nm * 12 + 64;
+  char* blk = nullptr;
+  AB2_CUDA(cudaMalloc(&blk, bytes));
+  P->block = blk;
+  P->seg_beg = reinterpret_cast<int64_t*>(blk);
+  P->seg_row = reinterpret_cast<int*>(blk + ns * 8);
+  P->seg_len = P->seg_row + ns;
+  P->seg_slot = P->seg_len + ns;
+  P->m_row = P->seg_slot + ns;
+  P->m_slot0 = P->m_row + nm;
+  P->m_nslot = P->m_slot0 + nm;
+  auto up = [&](void* d, const void* h, size_t n) {
+    if (n) AB2_CUDA(cudaMemcpy(d, h, n, cudaMemcpyHostToDevice));
+  };
+  up(P->seg_beg, beg.data(), beg.size() * 8);
+  up(P->seg_row, row.data(), row.size() * 4);
+  up(P->seg_len, len.data(), len.size() * 4);
+  up(P->seg_slot, slot.data(), slot.size() * 4);
+  up(P->m_row, mrow.data(), mrow.size() * 4);
+  up(P->m_slot0, mslot0.data(), mslot0.size() * 4);
+  up(P->m_nslot, mnslot.data(), mnslot.size() * 4);
+  const SegPlan& ref = *P;
+  m.emplace(S, std::move(P));
+  return ref;
+}
+
+std::pair<int64_t, int64_t> DevRatings::routing_totals(int n_blocks) {
+  auto it = routing.find(n_blocks);
+  if (it != routing.end()) return it->second;
+  unsigned long long* d = static_cast<unsigned long long*>(ctx->scratch(5, 16));
+  launch_routing_count(*this, n_blocks, d);
+  if (ctx->world > 1)
+    AB2_NCCL(ncclAllReduce(d, d, 2, ncclUint64, ncclSum, ctx->comm, ctx->stream));
+  unsigned long long h[2];
+  AB2_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  auto v = std::make_pair(static_cast<int64_t>(h[0]), static_cast<int64_t>(h[1]));
+  routing[n_blocks] = v;
+  return v;
+}
+
+}  // namespace ab2

@@ -1,0 +1,188 @@
+// engine.h -- internal device engine of the B200 ALS-NCG core.
+//
+// Owns the CUDA context state (device, stream, optional NCCL communicator,
+// scratch, per-kernel timing), the device-resident dual CSR/CSC store with
+// its work plans, and declares the kernel launchers implemented in k_*.cu.
+// Nothing here is part of the public ABI (include/alsncg_capi.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "alsncg_capi.h"
+
+namespace ab2 {
+
+// ---------------------------------------------------------------- errors --
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define AB2_CUDA(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::ab2::Error(e_ == cudaErrorMemoryAllocation ? ALSNCG_ENOMEM : ALSNCG_ECUDA, \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+
+#define AB2_NCCL(expr)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      throw ::ab2::Error(ALSNCG_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+inline int row_stride(int n_f) { return (n_f + 1) & ~1; }
+// Number of 8-wide blocks of the augmented Gram [m ; r] (rhs at column ld).
+inline int gram_blocks(int n_f) { return (row_stride(n_f) + 1 + 7) / 8; }
+constexpr int kMaxGramBlocks = 26;  // n_f <= 206
+constexpr int kMaxRank = 206;
+
+// -------------------------------------------------------------- context --
+struct KernelStat {
+  std::string name;
+  int64_t launches = 0;
+  double ms = 0.0;
+};
+
+struct Ctx {
+  int device = 0;
+  int rank = 0;
+  int world = 1;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  bool profiling = false;
+  int64_t launches = 0;
+  std::vector<KernelStat> stats;
+  struct Pending {
+    int stat;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  // Growable scratch slots (device), pinned host staging.
+  std::vector<void*> scratch_ptr;
+  std::vector<size_t> scratch_size;
+  double* d_red = nullptr;      // reduction partials (block-level, double-double)
+  unsigned* d_counters = nullptr;
+  double* d_scalars = nullptr;  // small result slots
+  double* h_scalars = nullptr;  // pinned mirror
+  int sm_count = 148;
+
+  explicit Ctx(int dev);
+  ~Ctx();
+  void* scratch(int slot, size_t bytes);
+  // Kernel launch bookkeeping: call before/after each launch.
+  int begin_launch(const char* name);
+  void end_launch(int token);
+  void collect_stats();  // syncs and folds pending events into stats
+  void sync();
+  void fetch_scalars(int n);  // d_scalars[0..n) -> h_scalars (synchronous)
+};
+
+// -------------------------------------------------------- device ratings --
+// One compressed view (CSR by user or CSC by item) restricted to this rank's
+// row range [row0, row0+nrows); ptr is rebased so ptr[0] == 0.
+struct View {
+  int row0 = 0;
+  int nrows = 0;
+  int64_t nnz = 0;
+  int64_t* ptr = nullptr;  // device, nrows+1
+  int* idx = nullptr;      // device, nnz
+  double* val = nullptr;   // device, nnz
+  std::vector<int64_t> h_ptr;  // host copy of ptr (plans are built on the host)
+};
+
+// Rows cut into segments of at most S ratings (heavy rows -> several
+// segments whose partials are reduced in segment order: deterministic).
+struct SegPlan {
+  int S = 0;
+  int n_seg = 0;
+  int n_multi = 0;  // rows with >1 segment
+  int n_slots = 0;  // segments belonging to multi rows
+  int* seg_row = nullptr;   // local row
+  int64_t* seg_beg = nullptr;
+  int* seg_len = nullptr;
+  int* seg_slot = nullptr;  // -1 for single-segment rows
+  int* m_row = nullptr;
+  int* m_slot0 = nullptr;
+  int* m_nslot = nullptr;
+  void* block = nullptr;  // single device allocation backing the arrays
+};
+
+constexpr int kTileRows = 64;  // quartic/loss tile height (rows per CTA)
+
+struct DevRatings {
+  Ctx* ctx = nullptr;
+  int n_u = 0, n_m = 0;
+  int64_t nnz = 0;
+  View users, items;
+  // Shard bounds of every rank (identical on all ranks).
+  std::vector<int> ub, mb;  // size world+1
+  std::map<int, std::unique_ptr<SegPlan>> plans[2];
+  std::map<int, std::pair<int64_t, int64_t>> routing;  // n_blocks -> (T_u, T_m)
+  ~DevRatings();
+  const View& view(int kind) const { return kind == 0 ? users : items; }
+  const SegPlan& plan(int kind, int S);
+  int n_rows(int kind) const { return kind == 0 ? n_u : n_m; }
+  std::pair<int64_t, int64_t> routing_totals(int n_blocks);
+};
+
+DevRatings* upload_ratings(Ctx* ctx, int n_u, int n_m, int64_t nnz, const int64_t* uptr,
+                           const int* uidx, const double* uval, const int64_t* iptr,
+                           const int* iidx, const double* ival);
+// nnz-balanced contiguous ranges aligned to `align` rows (identical on every rank).
+std::vector<int> partition_rows(int n_rows, const int64_t* ptr, int world, int align);
+
+// ------------------------------------------------------------- kernels --
+// All launchers enqueue on ctx->stream.  Device flat vectors: (n_u+n_m) rows
+// of ld = row_stride(n_f) doubles, user rows first.
+
+// Gradient rows of this rank's shard (both views) -> g (ncg.cpp:70-116).
+void launch_gradient(DevRatings& R, int n_f, const double* x, double lambda, double* g);
+// Tile partials of the quartic (linesearch.cpp:46-111) or of the loss
+// (ncg.cpp:43-68) for this rank's tiles; result reduced in global tile order
+// into ctx->d_scalars[slot..slot+5) (quartic) / [slot] (loss).
+void launch_quartic(DevRatings& R, int n_f, const double* x, const double* p, double lambda,
+                    int slot);
+void launch_loss(DevRatings& R, int n_f, const double* x, double lambda, int slot);
+// Half-sweep for this rank's rows of `kind` (0 users from item rows of src,
+// 1 items from user rows of src); writes rows of `out` (same flat layout).
+// Adds the number of least-norm fallback columns to d_counters[counter].
+void launch_half_sweep(DevRatings& R, int kind, int n_f, const double* src_rows,
+                       double lambda, double* out_rows, int counter);
+
+// Deterministic compensated reductions over n doubles.  Results land in
+// ctx->d_scalars[slot + k].
+enum VecOp {
+  kDot = 0,        // s0 = sum x*y
+  kGbarFused = 1,  // out = x - px; s0 = sum out*(g - gprev); s1 = sum out*g;
+                   // s2 = sum g*g; s3 = -sum g*out
+  kDirFused = 2,   // out = -gbar + beta*p; s0 = sum g*out
+  kBetaParts = 3,  // s0 = sum bn*(gn - gp); s1 = sum bp*gp
+};
+void launch_vec(Ctx* ctx, VecOp op, int64_t n, const double* a, const double* b,
+                const double* c, const double* d, double beta, double* out, int slot);
+// out = a*x + b*y elementwise (no FMA: reference rounding, factors.cpp:88-91).
+void launch_axpby(Ctx* ctx, int64_t n, double a, const double* x, double b, const double* y,
+                  double* out);
+// Routing-table totals (parallel.cpp:69-111) for this rank's rows.
+void launch_routing_count(DevRatings& R, int n_blocks, unsigned long long* d_out2);
+// Packed <-> padded row layout conversions.
+void launch_pad_rows(Ctx* ctx, int64_t rows, int n_f, const double* packed, double* padded);
+void launch_unpad_rows(Ctx* ctx, int64_t rows, int n_f, const double* padded, double* packed);
+
+// Multi-GPU: replicate row ranges [b[r], b[r+1]) of a row-major buffer from
+// their owning rank to all ranks (grouped in-place broadcasts over NCCL).
+void allgather_rows(Ctx* ctx, double* rows, const std::vector<int>& bounds, int ld);
+
+}  // namespace ab2

@@ -1,0 +1,600 @@
+// k_halfsweep.cu -- K1-K4: one ALS half-sweep (als.cpp:40-121,
+// parallel.cpp:144-185).  For every destination row c with ratings
+// {(j_t, r_t)}:
+//      (sum_t m_t m_t^T + lambda*n_c*I) u_c = sum_t r_t m_t ,  m_t = src row j_t
+// empty rows -> 0; unregularised or non-SPD systems -> least-norm solve.
+//
+// Design:
+//  * Rows are cut into segments of <= S ratings (SegPlan, heavy rows first).
+//    One group of GW warps owns a segment.  Gathered source rows are staged
+//    into shared memory with cp.async (16-byte, double-buffered, CH ratings
+//    per stage) as the augmented vector m' = [m, r] (rhs folded into the Gram).
+//  * Gram of m' on the FP64 tensor cores: mma.sync m8n8k4 f64 (SASS
+//    DMMA.8x8x4) over the NB(NB+1)/2 lower-triangular 8x8 blocks, k = 4
+//    ratings per MMA; block pairs are distributed round-robin over the warps,
+//    accumulators live in registers.
+//  * Single-segment rows finish in the same CTA: the Gram goes to shared
+//    memory, lambda*n_c is added to the diagonal and an in-place symmetric
+//    elimination (LDL^T form of Cholesky: a pivot <= 0 means "not SPD", as
+//    Eigen's LLT) runs on the augmented matrix, so the forward substitution
+//    falls out of the rhs row; one warp back-substitutes.
+//  * Multi-segment (heavy) rows write register partials per segment; a
+//    second kernel sums them in segment order (deterministic) and solves.
+//  * Fallback columns (lambda*n_c == 0 or a non-positive pivot) are listed
+//    and solved by k_hs_fallback: exact reference-order Gram, cyclic Jacobi
+//    eigen-decomposition, pseudo-inverse solve + one refinement step
+//    (als.cpp:71-81 semantics).
+#include "common.cuh"
+
+namespace ab2 {
+
+namespace {
+
+struct HsArgs {
+  const int64_t* ptr;
+  const int* idx;
+  const double* val;
+  int row0;            // flat-vector row of local row 0 (output side)
+  const double* src;   // flat-vector row 0 of the source side
+  double* out;         // flat vector base (rows indexed by row0 + local row)
+  int n_f, ld;
+  double lambda;
+  const int* seg_row;
+  const int64_t* seg_beg;
+  const int* seg_len;
+  const int* seg_slot;
+  int n_seg;
+  const int* m_row;
+  const int* m_slot0;
+  const int* m_nslot;
+  int n_multi;
+  double* partial;
+  int* fb_list;
+  unsigned* fb_count;
+  unsigned* fb_total;
+};
+
+template <int NB, int GW>
+struct HsCfg {
+  static constexpr int P = NB * (NB + 1) / 2;     // lower-triangular block pairs
+  static constexpr int Q = (P + GW - 1) / GW;     // pairs per warp
+  static constexpr int LDS = NB * 8 + 4;          // stage row stride (bank-conflict free)
+  static constexpr int CH = GW == 1 ? 16 : 32;    // ratings per stage
+  static constexpr bool PACKED = NB > 16;
+  static constexpr int MAXF = NB * 8;
+  static constexpr int GPC = GW == 1 ? 4 : 1;     // groups per CTA
+  static constexpr int THREADS = GW * 32 * GPC;
+  static constexpr int GT = GW * 32;              // threads per group
+  static constexpr int PART = GW * Q * 64;        // doubles per partial slot
+};
+
+template <int GW>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (GW == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+template <int NB, int GW>
+__host__ __device__ constexpr size_t hs_group_doubles(int ld) {
+  using C = HsCfg<NB, GW>;
+  const size_t stage = static_cast<size_t>(2) * C::CH * C::LDS;
+  const int lda = (ld + 1) | 1;
+  const size_t mat = C::PACKED ? static_cast<size_t>(ld + 1) * (ld + 2) / 2
+                               : static_cast<size_t>(ld + 1) * lda;
+  const size_t body = stage > mat ? stage : mat;
+  return body + 2 * static_cast<size_t>(C::MAXF);  // + dinv[], w[]
+}
+
+template <bool PACKED>
+__device__ __forceinline__ int midx(int i, int j, int lda) {
+  if constexpr (PACKED)
+    return i * (i + 1) / 2 + j;
+  else
+    return i * lda + j;
+}
+
+// Pair index p -> (I, J) with J <= I, row-major over the lower triangle.
+__device__ __forceinline__ void pair_ij(int p, int& I, int& J) {
+  int i = static_cast<int>((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= p) ++i;
+  while (i * (i + 1) / 2 > p) --i;
+  I = i;
+  J = p - i * (i + 1) / 2;
+}
+
+// Gram of the augmented rows over one segment, accumulated into acc.
+template <int NB, int GW>
+__device__ __forceinline__ void gram_segment(const HsArgs& a, double* S, int64_t beg, int len,
+                                             int gtid, int warp, int lane,
+                                             double (&acc)[HsCfg<NB, GW>::Q][2],
+                                             const int (&pI)[HsCfg<NB, GW>::Q],
+                                             const int (&pJ)[HsCfg<NB, GW>::Q]) {
+  using C = HsCfg<NB, GW>;
+  const int ld = a.ld;
+  const int nch = ld >> 1;  // 16-byte chunks per source row
+  double* buf[2] = {S, S + C::CH * C::LDS};
+  // zero the pad columns (ld, ld+1 .. NB*8) once; column ld carries r
+  for (int e = gtid; e < 2 * C::CH * (C::LDS - ld); e += C::GT) {
+    const int b = e / (C::CH * (C::LDS - ld));
+    const int rem = e % (C::CH * (C::LDS - ld));
+    const int t = rem / (C::LDS - ld), c = rem % (C::LDS - ld);
+    buf[b][t * C::LDS + ld + c] = 0.0;
+  }
+  group_sync<GW>();
+  auto issue = [&](int s, double* B) {
+    const int base = s * C::CH;
+    for (int c = gtid; c < C::CH * nch; c += C::GT) {
+      const int t = c / nch, k = c - t * nch;
+      const int rt = base + t;
+      double* dst = B + t * C::LDS + 2 * k;
+      if (rt < len) {
+        const int j = a.idx[beg + rt];
+        cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
+      } else {
+        *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+      }
+    }
+    for (int t = gtid; t < C::CH; t += C::GT) {
+      const int rt = base + t;
+      B[t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
+    }
+  };
+  const int nst = (len + C::CH - 1) / C::CH;
+  if (nst > 0) issue(0, buf[0]);
+  cp_async_commit();
+  for (int s = 0; s < nst; ++s) {
+    if (s + 1 < nst) {
+      issue(s + 1, buf[(s + 1) & 1]);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    group_sync<GW>();
+    const double* B = buf[s & 1];
+#pragma unroll 2
+    for (int kk = 0; kk < C::CH / 4; ++kk) {
+      const double* base = B + (kk * 4 + (lane & 3)) * C::LDS + (lane >> 2);
+#pragma unroll
+      for (int q = 0; q < C::Q; ++q) {
+        if (q < C::Q - 1 || warp + q * GW < C::P) {
+          const double av = base[8 * pI[q]];
+          const double bv = base[8 * pJ[q]];
+          dmma884(acc[q][0], acc[q][1], av, bv);
+        }
+      }
+    }
+    group_sync<GW>();
+  }
+}
+
+// Gram (in registers) -> shared matrix -> shifted elimination -> u.
+template <int NB, int GW>
+__device__ __forceinline__ void solve_row(const HsArgs& a, double* S, int lr, int count,
+                                          int gtid, int warp, int lane,
+                                          double (&acc)[HsCfg<NB, GW>::Q][2],
+                                          const int (&pI)[HsCfg<NB, GW>::Q],
+                                          const int (&pJ)[HsCfg<NB, GW>::Q]) {
+  using C = HsCfg<NB, GW>;
+  const int n_f = a.n_f, ld = a.ld;
+  const int lda = (ld + 1) | 1;
+  double* A = S;
+  const size_t body = hs_group_doubles<NB, GW>(ld) - 2 * C::MAXF;
+  double* dinv = S + body;
+  double* w = dinv + C::MAXF;
+  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+
+  group_sync<GW>();  // stage buffers are dead; A aliases them
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) {
+    if (q < C::Q - 1 || warp + q * GW < C::P) {
+      const int i = 8 * pI[q] + (lane >> 2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 8 * pJ[q] + 2 * (lane & 3) + e;
+        if (i <= ld && j <= i) A[midx<C::PACKED>(i, j, lda)] = acc[q][e];
+      }
+    }
+  }
+  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
+  group_sync<GW>();
+  bool ok = shift > 0.0;
+  if (ok) {
+    for (int d = gtid; d < n_f; d += C::GT) A[midx<C::PACKED>(d, d, lda)] += shift;
+    group_sync<GW>();
+    // Right-looking symmetric elimination on rows {0..n_f-1} U {ld}.
+    constexpr int TR = C::GT >= 128 ? 16 : 8;
+    constexpr int TC = C::GT / TR;
+    const int ti = gtid % TR, tj = gtid / TR;
+    for (int k = 0; k < n_f; ++k) {
+      const double d = A[midx<C::PACKED>(k, k, lda)];
+      if (!(d > 0.0)) {  // Eigen LLT reports NumericalIssue on pivot <= 0
+        ok = false;
+        break;
+      }
+      const double invd = 1.0 / d;
+      if (gtid == 0) dinv[k] = invd;
+      const int nreg = n_f - 1 - k;
+      for (int ii = ti; ii <= nreg; ii += TR) {
+        const int i = ii < nreg ? k + 1 + ii : ld;
+        const int jmax = ii < nreg ? i : n_f - 1;
+        const double s = A[midx<C::PACKED>(i, k, lda)] * invd;
+        for (int j = k + 1 + tj; j <= jmax; j += TC)
+          A[midx<C::PACKED>(i, j, lda)] =
+              fma(-s, A[midx<C::PACKED>(j, k, lda)], A[midx<C::PACKED>(i, j, lda)]);
+      }
+      group_sync<GW>();
+    }
+  }
+  if (!ok) {
+    if (gtid == 0) {
+      const unsigned slot = atomicAdd(a.fb_count, 1u);
+      a.fb_list[slot] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  // Back substitution (warp 0): u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
+  if (warp == 0) {
+    for (int i = lane; i < n_f; i += 32) w[i] = A[midx<C::PACKED>(ld, i, lda)];
+    __syncwarp();
+    for (int k = n_f - 1; k >= 0; --k) {
+      const double u = w[k] * dinv[k];
+      for (int i = lane; i < k; i += 32) w[i] = fma(-A[midx<C::PACKED>(k, i, lda)], u, w[i]);
+      if (lane == 0) out[k] = u;
+      __syncwarp();
+    }
+    if (lane == 0 && ld > n_f) out[n_f] = 0.0;
+  }
+}
+
+template <int NB, int GW>
+__device__ __forceinline__ void init_pairs(int warp, int (&pI)[HsCfg<NB, GW>::Q],
+                                           int (&pJ)[HsCfg<NB, GW>::Q],
+                                           double (&acc)[HsCfg<NB, GW>::Q][2]) {
+  using C = HsCfg<NB, GW>;
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) {
+    const int p = warp + q * GW;
+    int I = 0, J = 0;
+    if (p < C::P) pair_ij(p, I, J);
+    pI[q] = I;
+    pJ[q] = J;
+    acc[q][0] = 0.0;
+    acc[q][1] = 0.0;
+  }
+}
+
+template <int NB, int GW>
+__global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
+  using C = HsCfg<NB, GW>;
+  extern __shared__ __align__(16) double smem[];
+  const int group = threadIdx.x / C::GT;
+  const int gtid = threadIdx.x % C::GT;
+  const int warp = gtid >> 5, lane = gtid & 31;
+  const int seg = blockIdx.x * C::GPC + group;
+  if (seg >= a.n_seg) return;  // uniform per group (GW==1 groups are warps)
+  double* S = smem + static_cast<size_t>(group) * hs_group_doubles<NB, GW>(a.ld);
+  const int lr = a.seg_row[seg];
+  const int len = a.seg_len[seg];
+  const int slot = a.seg_slot[seg];
+  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * a.ld;
+  if (len == 0) {  // zero-rating column stays zero (parallel.cpp:175)
+    for (int k = gtid; k < a.ld; k += C::GT) out[k] = 0.0;
+    return;
+  }
+  int pI[C::Q], pJ[C::Q];
+  double acc[C::Q][2];
+  init_pairs<NB, GW>(warp, pI, pJ, acc);
+  gram_segment<NB, GW>(a, S, a.seg_beg[seg], len, gtid, warp, lane, acc, pI, pJ);
+  if (slot >= 0) {
+    double* P = a.partial + static_cast<int64_t>(slot) * C::PART;
+#pragma unroll
+    for (int q = 0; q < C::Q; ++q)
+      *reinterpret_cast<double2*>(P + (warp * C::Q + q) * 64 + lane * 2) =
+          make_double2(acc[q][0], acc[q][1]);
+    return;
+  }
+  solve_row<NB, GW>(a, S, lr, len, gtid, warp, lane, acc, pI, pJ);
+}
+
+template <int NB, int GW>
+__global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) {
+  using C = HsCfg<NB, GW>;
+  extern __shared__ __align__(16) double smem[];
+  const int group = threadIdx.x / C::GT;
+  const int gtid = threadIdx.x % C::GT;
+  const int warp = gtid >> 5, lane = gtid & 31;
+  const int m = blockIdx.x * C::GPC + group;
+  if (m >= a.n_multi) return;
+  double* S = smem + static_cast<size_t>(group) * hs_group_doubles<NB, GW>(a.ld);
+  int pI[C::Q], pJ[C::Q];
+  double acc[C::Q][2];
+  init_pairs<NB, GW>(warp, pI, pJ, acc);
+  const int slot0 = a.m_slot0[m], ns = a.m_nslot[m];
+  for (int s = 0; s < ns; ++s) {  // segment order -> deterministic
+    const double* P = a.partial + static_cast<int64_t>(slot0 + s) * C::PART;
+#pragma unroll
+    for (int q = 0; q < C::Q; ++q) {
+      const double2 v = *reinterpret_cast<const double2*>(P + (warp * C::Q + q) * 64 + lane * 2);
+      acc[q][0] += v.x;
+      acc[q][1] += v.y;
+    }
+  }
+  const int lr = a.m_row[m];
+  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
+  solve_row<NB, GW>(a, S, lr, count, gtid, warp, lane, acc, pI, pJ);
+}
+
+// ------------------------------------------------------------ fallback --
+// Least-norm solve for listed rows.  Workspace per CTA: W (n x n), Q (n x n).
+constexpr int kFbThreads = 256;
+constexpr int kFbBlocks = 32;
+
+__device__ void fb_block_sum2(double& a, double& b, double* sh) {
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(kFull, a, off);
+    b += __shfl_xor_sync(kFull, b, off);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[2 * warp] = a;
+    sh[2 * warp + 1] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0, y = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+      x += sh[2 * w2];
+      y += sh[2 * w2 + 1];
+    }
+    sh[64] = x;
+    sh[65] = y;
+  }
+  __syncthreads();
+  a = sh[64];
+  b = sh[65];
+  __syncthreads();
+}
+
+// out = pinv(W-eigen) * rhs, using eigenvalues on W's diagonal and vectors in Q.
+__device__ void fb_pinv_apply(int n, const double* W, const double* Q, const double* rhs,
+                              double* out, double* tmp, double* sh) {
+  double emax = 0.0, dummy = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) emax = fmax(emax, fabs(W[i * n + i]));
+  // block max via sum trick: reuse fb_block_sum2 with max semantics
+  for (int off = 16; off > 0; off >>= 1) emax = fmax(emax, __shfl_xor_sync(kFull, emax, off));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = emax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) m = fmax(m, sh[w2]);
+    sh[64] = m;
+  }
+  __syncthreads();
+  emax = sh[64];
+  __syncthreads();
+  (void)dummy;
+  const double thresh = emax * n * 2.220446049250313e-16;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const double lam = W[e * n + e];
+    double proj = 0.0;
+    if (fabs(lam) > thresh) {
+      for (int k = 0; k < n; ++k) proj += Q[k * n + e] * rhs[k];
+      proj /= lam;
+    }
+    tmp[e] = proj;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    double s = 0.0;
+    for (int e = 0; e < n; ++e) s += tmp[e] * Q[k * n + e];
+    out[k] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFbThreads) k_hs_fallback(HsArgs a, double* work) {
+  const int n = a.n_f, ld = a.ld;
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* A = work + blockIdx.x * (3 * nn + 6 * static_cast<size_t>(n));
+  double* W = A + nn;
+  double* Q = W + nn;
+  double* v = Q + nn;
+  double* u = v + n;
+  double* res = u + n;
+  double* du = res + n;
+  double* tmp = du + n;
+  __shared__ double sh[80];
+  __shared__ double rot[2];
+  const unsigned total = *a.fb_count;
+  for (unsigned f = blockIdx.x; f < total; f += gridDim.x) {
+    const int lr = a.fb_list[f];
+    const int64_t b = a.ptr[lr];
+    const int count = static_cast<int>(a.ptr[lr + 1] - b);
+    // Gram + rhs in the reference's summation order (als.cpp:49-57), no FMA.
+    for (size_t e = threadIdx.x; e < nn + n; e += blockDim.x) {
+      double s = 0.0;
+      if (e < nn) {
+        const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+        const int lo = j <= i ? j : i, hi = j <= i ? i : j;
+        for (int t = 0; t < count; ++t) {
+          const double* m = a.src + static_cast<int64_t>(a.idx[b + t]) * ld;
+          s = __dadd_rn(s, __dmul_rn(m[hi], m[lo]));
+        }
+        if (i == j) s = __dadd_rn(s, a.lambda * count);
+        A[e] = s;
+        W[e] = s;
+        Q[e] = i == j ? 1.0 : 0.0;
+      } else {
+        const int i = static_cast<int>(e - nn);
+        for (int t = 0; t < count; ++t) {
+          const double* m = a.src + static_cast<int64_t>(a.idx[b + t]) * ld;
+          s = __dadd_rn(s, __dmul_rn(a.val[b + t], m[i]));
+        }
+        v[i] = s;
+      }
+    }
+    __syncthreads();
+    // cyclic Jacobi (same sweep structure as the oracle restatement)
+    for (int sweep = 0; sweep < 100; ++sweep) {
+      double off = 0.0, tot = 0.0;
+      for (size_t e = threadIdx.x; e < nn; e += blockDim.x) {
+        const double x = W[e] * W[e];
+        tot += x;
+        if (e / n != e % n) off += x;
+      }
+      fb_block_sum2(off, tot, sh);
+      if (off <= 1e-30 * tot || off == 0.0) break;
+      for (int p = 0; p < n; ++p)
+        for (int r = p + 1; r < n; ++r) {
+          if (threadIdx.x == 0) {
+            const double apr = W[p * n + r];
+            if (apr == 0.0) {
+              rot[0] = 1.0;
+              rot[1] = 0.0;
+            } else {
+              const double app = W[p * n + p], arr = W[r * n + r];
+              const double theta = (arr - app) / (2.0 * apr);
+              const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+              const double c = 1.0 / sqrt(t * t + 1.0);
+              rot[0] = c;
+              rot[1] = t * c;
+            }
+          }
+          __syncthreads();
+          const double c = rot[0], s = rot[1];
+          if (s != 0.0) {
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+              const double wkp = W[k * n + p], wkr = W[k * n + r];
+              W[k * n + p] = c * wkp - s * wkr;
+              W[k * n + r] = s * wkp + c * wkr;
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+              const double wpk = W[p * n + k], wrk = W[r * n + k];
+              W[p * n + k] = c * wpk - s * wrk;
+              W[r * n + k] = s * wpk + c * wrk;
+              const double qkp = Q[k * n + p], qkr = Q[k * n + r];
+              Q[k * n + p] = c * qkp - s * qkr;
+              Q[k * n + r] = s * qkp + c * qkr;
+            }
+          }
+          __syncthreads();
+        }
+    }
+    fb_pinv_apply(n, W, Q, v, u, tmp, sh);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // one refinement step (als.cpp:79)
+      double s = 0.0;
+      for (int k = 0; k < n; ++k) s += A[i * n + k] * u[k];
+      res[i] = v[i] - s;
+    }
+    __syncthreads();
+    fb_pinv_apply(n, W, Q, res, du, tmp, sh);
+    double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+    for (int i = threadIdx.x; i < ld; i += blockDim.x) out[i] = i < n ? u[i] + du[i] : 0.0;
+    __syncthreads();
+  }
+}
+
+template <int NB>
+struct Mode {
+  static constexpr int GW = NB <= 4 ? 1 : (NB <= 16 ? 4 : 8);
+};
+
+template <int NB>
+void run_hs(Ctx* ctx, HsArgs& a, const SegPlan& P) {
+  constexpr int GW = Mode<NB>::GW;
+  using C = HsCfg<NB, GW>;
+  const size_t smem = sizeof(double) * hs_group_doubles<NB, GW>(a.ld) * C::GPC;
+  static bool attr_set = false;
+  if (!attr_set) {
+    AB2_CUDA(cudaFuncSetAttribute(k_hs_main<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    AB2_CUDA(cudaFuncSetAttribute(k_hs_reduce<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr_set = true;
+  }
+  if (P.n_slots > 0)
+    a.partial = static_cast<double*>(ctx->scratch(2, sizeof(double) * C::PART * P.n_slots));
+  {
+    const int blocks = (P.n_seg + C::GPC - 1) / C::GPC;
+    const int tok = ctx->begin_launch("halfsweep_gram_solve");
+    k_hs_main<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
+    ctx->end_launch(tok);
+  }
+  if (P.n_multi > 0) {
+    const int blocks = (P.n_multi + C::GPC - 1) / C::GPC;
+    const int tok = ctx->begin_launch("halfsweep_reduce_solve");
+    k_hs_reduce<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
+    ctx->end_launch(tok);
+  }
+}
+
+int hs_segment_size(int n_f) {
+  if (n_f <= 32) return 8192;
+  if (n_f <= 64) return 4096;
+  return 2048;
+}
+
+}  // namespace
+
+void launch_half_sweep(DevRatings& R, int kind, int n_f, const double* src_rows, double lambda,
+                       double* out_rows, int counter) {
+  Ctx* ctx = R.ctx;
+  if (n_f > kMaxRank) throw Error(ALSNCG_EUNSUPPORTED, "n_f exceeds the half-sweep kernel range");
+  const View& v = R.view(kind);
+  if (v.nrows == 0) return;
+  const int ld = row_stride(n_f);
+  const SegPlan& P = R.plan(kind, hs_segment_size(n_f));
+  HsArgs a;
+  a.ptr = v.ptr;
+  a.idx = v.idx;
+  a.val = v.val;
+  a.row0 = (kind == 0 ? 0 : R.n_u) + v.row0;
+  a.src = src_rows;
+  a.out = out_rows;
+  a.n_f = n_f;
+  a.ld = ld;
+  a.lambda = lambda;
+  a.seg_row = P.seg_row;
+  a.seg_beg = P.seg_beg;
+  a.seg_len = P.seg_len;
+  a.seg_slot = P.seg_slot;
+  a.n_seg = P.n_seg;
+  a.m_row = P.m_row;
+  a.m_slot0 = P.m_slot0;
+  a.m_nslot = P.m_nslot;
+  a.n_multi = P.n_multi;
+  a.partial = nullptr;
+  // fallback bookkeeping: counters[2+...] region
+  unsigned* fb_count = ctx->d_counters + 8;
+  a.fb_list = static_cast<int*>(ctx->scratch(3, sizeof(int) * std::max(v.nrows, 1)));
+  a.fb_count = fb_count;
+  a.fb_total = ctx->d_counters + counter;
+  AB2_CUDA(cudaMemsetAsync(fb_count, 0, sizeof(unsigned), ctx->stream));
+  switch (gram_blocks(n_f)) {
+#define AB2_HS_CASE(NB) \
+  case NB:              \
+    run_hs<NB>(ctx, a, P); \
+    break;
+    AB2_HS_CASE(1) AB2_HS_CASE(2) AB2_HS_CASE(3) AB2_HS_CASE(4) AB2_HS_CASE(5) AB2_HS_CASE(6)
+    AB2_HS_CASE(7) AB2_HS_CASE(8) AB2_HS_CASE(9) AB2_HS_CASE(10) AB2_HS_CASE(11) AB2_HS_CASE(12)
+    AB2_HS_CASE(13) AB2_HS_CASE(14) AB2_HS_CASE(15) AB2_HS_CASE(16) AB2_HS_CASE(17)
+    AB2_HS_CASE(18) AB2_HS_CASE(19) AB2_HS_CASE(20) AB2_HS_CASE(21) AB2_HS_CASE(22)
+    AB2_HS_CASE(23) AB2_HS_CASE(24) AB2_HS_CASE(25) AB2_HS_CASE(26)
+#undef AB2_HS_CASE
+    default:
+      throw Error(ALSNCG_EUNSUPPORTED, "n_f exceeds the half-sweep kernel range");
+  }
+  // Fallback pass (no host sync: the kernel reads the device-side count).
+  const size_t per = 3 * static_cast<size_t>(n_f) * n_f + 6 * static_cast<size_t>(n_f);
+  double* work = static_cast<double*>(ctx->scratch(4, sizeof(double) * per * kFbBlocks));
+  const int tok = ctx->begin_launch("halfsweep_fallback");
+  k_hs_fallback<<<kFbBlocks, kFbThreads, 0, ctx->stream>>>(a, work);
+  ctx->end_launch(tok);
+}
+
+}  // namespace ab2

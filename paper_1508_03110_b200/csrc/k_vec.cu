@@ -1,0 +1,236 @@
+// k_vec.cu -- K8: fused NCG vector work (ncg.cpp:118-136, 186-275;
+// factors.cpp:80-105) as single-pass kernels with deterministic compensated
+// reductions, plus layout helpers and the routing-table counter.
+//
+// Elementwise results are bit-identical to the reference (each op is one
+// IEEE multiply or add in the reference's order, no FMA); reductions are
+// double-double per thread -> block -> last-block finalise in block order.
+// Roofline: HBM-bound; algorithmic bytes = 8 B x (#streams read + written)
+// per element (K8).
+#include "common.cuh"
+
+namespace ab2 {
+
+namespace {
+
+constexpr int kVecThreads = 256;
+constexpr int kVecMaxBlocks = 4 * 148;
+
+template <int OP>
+struct VecNS {
+  static constexpr int value = OP == kDot ? 1 : OP == kGbarFused ? 4 : OP == kDirFused ? 1 : 2;
+};
+
+template <int OP>
+__device__ __forceinline__ void vec_elem(int64_t i, const double* __restrict__ a,
+                                         const double* __restrict__ b,
+                                         const double* __restrict__ c,
+                                         const double* __restrict__ d, double beta,
+                                         double* __restrict__ out, dd (&acc)[VecNS<OP>::value]) {
+  if constexpr (OP == kDot) {
+    dd_add(acc[0], __dmul_rn(a[i], b[i]));
+  } else if constexpr (OP == kGbarFused) {
+    // gbar_next = 1*x_next + (-1)*P(x_next)         (ncg.cpp:257)
+    const double g = c[i];
+    const double o = __dsub_rn(a[i], b[i]);
+    out[i] = o;
+    dd_add(acc[0], __dmul_rn(o, __dsub_rn(g, d[i])));  // beta numerator   (ncg.cpp:126-129)
+    dd_add(acc[1], __dmul_rn(o, g));                   // next denominator (ncg.cpp:123)
+    dd_add(acc[2], __dmul_rn(g, g));                   // ||g||^2          (ncg.cpp:134-136)
+    dd_add(acc[3], __dmul_rn(g, -o));                  // g.p for p=-gbar  (ncg.cpp:270)
+  } else if constexpr (OP == kDirFused) {
+    // p_next = -1*gbar_next + beta*p                   (ncg.cpp:267)
+    const double o = __dadd_rn(-a[i], __dmul_rn(beta, b[i]));
+    out[i] = o;
+    dd_add(acc[0], __dmul_rn(c[i], o));                // g_next.p_next    (ncg.cpp:270)
+  } else {
+    dd_add(acc[0], __dmul_rn(a[i], __dsub_rn(b[i], c[i])));
+    dd_add(acc[1], __dmul_rn(d[i], c[i]));
+  }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kVecThreads)
+    k_vec(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+          const double* __restrict__ c, const double* __restrict__ d, double beta,
+          double* __restrict__ out, dd* __restrict__ partials, unsigned* counter,
+          double* result) {
+  constexpr int NS = VecNS<OP>::value;
+  __shared__ dd sh[(kVecThreads / 32) * NS];
+  __shared__ bool last;
+  dd acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = {0.0, 0.0};
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    vec_elem<OP>(i, a, b, c, d, beta, out, acc);
+  block_sum_dd<NS>(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) partials[blockIdx.x * NS + k] = acc[k];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = {0.0, 0.0};
+  for (int blk = threadIdx.x; blk < gridDim.x; blk += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const volatile dd* p = partials + blk * NS + k;
+      acc[k] = dd_plus(acc[k], dd{p->hi, p->lo});
+    }
+  block_sum_dd<NS>(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) result[k] = dd_value(acc[k]);
+    *counter = 0u;
+  }
+}
+
+__global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
+}
+
+__global__ void k_pad_rows(int64_t rows, int n_f, int ld, const double* __restrict__ packed,
+                           double* __restrict__ padded) {
+  const int64_t n = rows * ld;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = i / ld;
+    const int k = static_cast<int>(i - r * ld);
+    padded[i] = k < n_f ? packed[r * n_f + k] : 0.0;
+  }
+}
+
+__global__ void k_unpad_rows(int64_t rows, int n_f, int ld, const double* __restrict__ padded,
+                             double* __restrict__ packed) {
+  const int64_t n = rows * n_f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = i / n_f;
+    const int k = static_cast<int>(i - r * n_f);
+    packed[i] = padded[r * ld + k];
+  }
+}
+
+// parallel.cpp:69-111: a column is listed once per distinct destination
+// block among its neighbours; totals = sum over rows of #distinct(idx % nb).
+__global__ void k_routing_count(int nrows, const int64_t* __restrict__ ptr,
+                                const int* __restrict__ idx, int nb,
+                                unsigned long long* __restrict__ out) {
+  extern __shared__ unsigned bits[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int words = (nb + 31) / 32;
+  unsigned* my = bits + warp * words;
+  unsigned long long total = 0;
+  for (int r = blockIdx.x * (blockDim.x / 32) + warp; r < nrows; r += gridDim.x * (blockDim.x / 32)) {
+    for (int w = lane; w < words; w += 32) my[w] = 0u;
+    __syncwarp();
+    for (int64_t t = ptr[r] + lane; t < ptr[r + 1]; t += 32) {
+      const int d = idx[t] % nb;
+      atomicOr(&my[d >> 5], 1u << (d & 31));
+    }
+    __syncwarp();
+    int c = 0;
+    for (int w = lane; w < words; w += 32) c += __popc(my[w]);
+    total += static_cast<unsigned long long>(c);
+    __syncwarp();
+  }
+  for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(kFull, total, off);
+  if (lane == 0) atomicAdd(out, total);
+}
+
+int vec_blocks(int64_t n) {
+  int64_t b = (n + kVecThreads * 8 - 1) / (kVecThreads * 8);
+  if (b < 1) b = 1;
+  if (b > kVecMaxBlocks) b = kVecMaxBlocks;
+  return static_cast<int>(b);
+}
+
+int ew_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return static_cast<int>(b);
+}
+
+}  // namespace
+
+void launch_vec(Ctx* ctx, VecOp op, int64_t n, const double* a, const double* b, const double* c,
+                const double* d, double beta, double* out, int slot) {
+  const int blocks = vec_blocks(n);
+  dd* partials = reinterpret_cast<dd*>(ctx->d_red);
+  double* res = ctx->d_scalars + slot;
+  unsigned* cnt = ctx->d_counters;
+  switch (op) {
+    case kDot: {
+      const int t = ctx->begin_launch("vec_dot");
+      k_vec<kDot><<<blocks, kVecThreads, 0, ctx->stream>>>(n, a, b, c, d, beta, out, partials, cnt, res);
+      ctx->end_launch(t);
+      break;
+    }
+    case kGbarFused: {
+      const int t = ctx->begin_launch("vec_gbar_fused");
+      k_vec<kGbarFused><<<blocks, kVecThreads, 0, ctx->stream>>>(n, a, b, c, d, beta, out, partials, cnt, res);
+      ctx->end_launch(t);
+      break;
+    }
+    case kDirFused: {
+      const int t = ctx->begin_launch("vec_dir_fused");
+      k_vec<kDirFused><<<blocks, kVecThreads, 0, ctx->stream>>>(n, a, b, c, d, beta, out, partials, cnt, res);
+      ctx->end_launch(t);
+      break;
+    }
+    case kBetaParts: {
+      const int t = ctx->begin_launch("vec_beta_parts");
+      k_vec<kBetaParts><<<blocks, kVecThreads, 0, ctx->stream>>>(n, a, b, c, d, beta, out, partials, cnt, res);
+      ctx->end_launch(t);
+      break;
+    }
+  }
+}
+
+void launch_axpby(Ctx* ctx, int64_t n, double a, const double* x, double b, const double* y,
+                  double* out) {
+  const int t = ctx->begin_launch("vec_axpby");
+  k_axpby<<<ew_blocks(n), 256, 0, ctx->stream>>>(n, a, x, b, y, out);
+  ctx->end_launch(t);
+}
+
+void launch_pad_rows(Ctx* ctx, int64_t rows, int n_f, const double* packed, double* padded) {
+  const int t = ctx->begin_launch("pad_rows");
+  k_pad_rows<<<ew_blocks(rows * row_stride(n_f)), 256, 0, ctx->stream>>>(rows, n_f, row_stride(n_f),
+                                                                          packed, padded);
+  ctx->end_launch(t);
+}
+
+void launch_unpad_rows(Ctx* ctx, int64_t rows, int n_f, const double* padded, double* packed) {
+  const int t = ctx->begin_launch("unpad_rows");
+  k_unpad_rows<<<ew_blocks(rows * n_f), 256, 0, ctx->stream>>>(rows, n_f, row_stride(n_f), padded,
+                                                               packed);
+  ctx->end_launch(t);
+}
+
+void launch_routing_count(DevRatings& R, int n_blocks, unsigned long long* d_out2) {
+  Ctx* ctx = R.ctx;
+  AB2_CUDA(cudaMemsetAsync(d_out2, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  const int words = (n_blocks + 31) / 32;
+  const size_t smem = static_cast<size_t>(8) * words * sizeof(unsigned);
+  // T_u: user columns -> item destination blocks (neighbours are items).
+  for (int kind = 0; kind < 2; ++kind) {
+    const View& v = R.view(kind);
+    if (v.nrows == 0) continue;
+    const int blocks = std::min(148 * 8, (v.nrows + 7) / 8);
+    const int t = ctx->begin_launch("routing_count");
+    k_routing_count<<<blocks, 256, smem, ctx->stream>>>(v.nrows, v.ptr, v.idx, n_blocks, d_out2 + kind);
+    ctx->end_launch(t);
+  }
+}
+
+}  // namespace ab2
