@@ -197,6 +197,8 @@ DevRatings::~DevRatings() {
   free_view(items);
   for (auto& m : plans)
     for (auto& kv : m) cudaFree(kv.second->block);
+  for (auto& m : hs_plans)
+    for (auto& kv : m) cudaFree(kv.second->block);
 }
 
 const SegPlan& DevRatings::plan(int kind, int S) {
@@ -267,6 +269,86 @@ const SegPlan& DevRatings::plan(int kind, int S) {
   up(P->m_nslot, mnslot.data(), mnslot.size() * 4);
   const SegPlan& ref = *P;
   m.emplace(S, std::move(P));
+  return ref;
+}
+
+const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
+  auto key = std::make_pair(S, max_slots);
+  auto& m = hs_plans[kind];
+  auto it = m.find(key);
+  if (it != m.end()) return *it->second;
+  const View& v = view(kind);
+  auto P = std::make_unique<HsPlan>();
+  P->S = S;
+  std::vector<int> row_slot0(std::max(v.nrows, 1), 0), row_nslot(std::max(v.nrows, 1), 0);
+  std::vector<int> srow, slen, sslot;
+  std::vector<int64_t> sbeg;
+  int r = 0;
+  while (r < v.nrows) {
+    HsBatch b;
+    b.row0 = r;
+    b.seg0 = static_cast<int>(srow.size());
+    int slots = 0;
+    std::vector<int> order;  // segment ids of this batch
+    const size_t first = srow.size();
+    while (r < v.nrows) {
+      const int64_t c = v.h_ptr[r + 1] - v.h_ptr[r];
+      const int ns = c == 0 ? 0 : static_cast<int>((c + S - 1) / S);
+      if (slots > 0 && slots + ns > max_slots) break;
+      row_slot0[r] = slots;
+      row_nslot[r] = ns;
+      for (int s2 = 0; s2 < ns; ++s2) {
+        srow.push_back(r);
+        sbeg.push_back(v.h_ptr[r] + static_cast<int64_t>(s2) * S);
+        slen.push_back(static_cast<int>(std::min<int64_t>(S, c - static_cast<int64_t>(s2) * S)));
+        sslot.push_back(slots + s2);
+      }
+      slots += ns;
+      ++r;
+    }
+    // heavy-first order inside the batch (load balance of the Gram kernel)
+    std::vector<int> perm(srow.size() - first);
+    std::iota(perm.begin(), perm.end(), static_cast<int>(first));
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b2) { return slen[a] > slen[b2]; });
+    std::vector<int> r2, l2, s2v;
+    std::vector<int64_t> b2v;
+    for (int id : perm) {
+      r2.push_back(srow[id]);
+      l2.push_back(slen[id]);
+      s2v.push_back(sslot[id]);
+      b2v.push_back(sbeg[id]);
+    }
+    std::copy(r2.begin(), r2.end(), srow.begin() + first);
+    std::copy(l2.begin(), l2.end(), slen.begin() + first);
+    std::copy(s2v.begin(), s2v.end(), sslot.begin() + first);
+    std::copy(b2v.begin(), b2v.end(), sbeg.begin() + first);
+    b.row1 = r;
+    b.seg1 = static_cast<int>(srow.size());
+    b.nslots = slots;
+    P->max_batch_slots = std::max(P->max_batch_slots, slots);
+    P->batches.push_back(b);
+  }
+  const size_t ns = std::max<size_t>(srow.size(), 1), nr = std::max<size_t>(v.nrows, 1);
+  char* blk = nullptr;
+  AB2_CUDA(cudaMalloc(&blk, ns * (8 + 4 + 4 + 4) + nr * 8 + 64));
+  P->block = blk;
+  P->seg_beg = reinterpret_cast<int64_t*>(blk);
+  P->seg_row = reinterpret_cast<int*>(blk + ns * 8);
+  P->seg_len = P->seg_row + ns;
+  P->seg_slot = P->seg_len + ns;
+  P->row_slot0 = P->seg_slot + ns;
+  P->row_nslot = P->row_slot0 + nr;
+  auto up = [&](void* d, const void* h, size_t n) {
+    if (n) AB2_CUDA(cudaMemcpy(d, h, n, cudaMemcpyHostToDevice));
+  };
+  up(P->seg_beg, sbeg.data(), sbeg.size() * 8);
+  up(P->seg_row, srow.data(), srow.size() * 4);
+  up(P->seg_len, slen.data(), slen.size() * 4);
+  up(P->seg_slot, sslot.data(), sslot.size() * 4);
+  up(P->row_slot0, row_slot0.data(), static_cast<size_t>(v.nrows) * 4);
+  up(P->row_nslot, row_nslot.data(), static_cast<size_t>(v.nrows) * 4);
+  const HsPlan& ref = *P;
+  m.emplace(key, std::move(P));
   return ref;
 }
 

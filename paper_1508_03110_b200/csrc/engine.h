@@ -121,6 +121,28 @@ struct SegPlan {
 
 constexpr int kTileRows = 64;  // quartic/loss tile height (rows per CTA)
 
+// Half-sweep work plan for the split Gram / solve kernels: rows are grouped
+// into batches whose partial-Gram slots fit a memory budget; within a batch
+// every segment owns one slot, a row's slots are contiguous (row_slot0,
+// row_nslot, local to the batch) and segments are ordered heavy-first.
+struct HsBatch {
+  int row0, row1;  // local rows [row0, row1)
+  int seg0, seg1;  // segments of the batch
+  int nslots;
+};
+struct HsPlan {
+  int S = 0;
+  std::vector<HsBatch> batches;
+  int* seg_row = nullptr;
+  int64_t* seg_beg = nullptr;
+  int* seg_len = nullptr;
+  int* seg_slot = nullptr;
+  int* row_slot0 = nullptr;
+  int* row_nslot = nullptr;
+  int max_batch_slots = 0;
+  void* block = nullptr;
+};
+
 struct DevRatings {
   Ctx* ctx = nullptr;
   int n_u = 0, n_m = 0;
@@ -129,10 +151,12 @@ struct DevRatings {
   // Shard bounds of every rank (identical on all ranks).
   std::vector<int> ub, mb;  // size world+1
   std::map<int, std::unique_ptr<SegPlan>> plans[2];
+  std::map<std::pair<int, int64_t>, std::unique_ptr<HsPlan>> hs_plans[2];
   std::map<int, std::pair<int64_t, int64_t>> routing;  // n_blocks -> (T_u, T_m)
   ~DevRatings();
   const View& view(int kind) const { return kind == 0 ? users : items; }
   const SegPlan& plan(int kind, int S);
+  const HsPlan& hs_plan(int kind, int S, int64_t max_slots);
   int n_rows(int kind) const { return kind == 0 ? n_u : n_m; }
   std::pair<int64_t, int64_t> routing_totals(int n_blocks);
 };

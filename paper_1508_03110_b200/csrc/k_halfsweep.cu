@@ -123,17 +123,22 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, double* S, int64_t
     buf[b][t * C::LDS + ld + c] = 0.0;
   }
   group_sync<GW>();
+  // Each warp loads the stage's CH indices with one coalesced load (lane t
+  // holds rating t) and hands them out by shuffle, so every cp.async of the
+  // stage issues after a single index-load latency.
   auto issue = [&](int s, double* B) {
     const int base = s * C::CH;
-    for (int c = gtid; c < C::CH * nch; c += C::GT) {
-      const int t = c / nch, k = c - t * nch;
-      const int rt = base + t;
-      double* dst = B + t * C::LDS + 2 * k;
-      if (rt < len) {
-        const int j = a.idx[beg + rt];
-        cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
-      } else {
-        *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+    const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
+    for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
+      const int c = c0 + gtid;
+      const int t = min(c / nch, C::CH - 1), k = c - t * nch;
+      const int j = __shfl_sync(kFull, jv, t);
+      if (c < C::CH * nch) {
+        double* dst = B + t * C::LDS + 2 * k;
+        if (base + t < len)
+          cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
+        else
+          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
       }
     }
     for (int t = gtid; t < C::CH; t += C::GT) {
@@ -328,6 +333,199 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
   solve_row<NB, GW>(a, S, lr, count, gtid, warp, lane, acc, pI, pJ);
 }
 
+// ------------------------------------------------ split path (n_f >= 31) --
+// K1/K2: Gram-only kernel.  One CTA of W warps per segment; the augmented
+// Gram of the segment is written as NB(NB+1)/2 canonical 8x8 blocks in
+// C-fragment order (lane-major, 64 doubles per block) to its slot.
+template <int NB, int W>
+__global__ void __launch_bounds__(W * 32) k_hs_gram(HsArgs a, const int* __restrict__ seg_len,
+                                                    const int64_t* __restrict__ seg_beg,
+                                                    const int* __restrict__ seg_slot,
+                                                    double* __restrict__ G) {
+  using C = HsCfg<NB, W>;
+  extern __shared__ __align__(16) double smem[];
+  const int gtid = threadIdx.x, warp = gtid >> 5, lane = gtid & 31;
+  const int seg = blockIdx.x;
+  int pI[C::Q], pJ[C::Q];
+  double acc[C::Q][2];
+  init_pairs<NB, W>(warp, pI, pJ, acc);
+  gram_segment<NB, W>(a, smem, seg_beg[seg], seg_len[seg], gtid, warp, lane, acc, pI, pJ);
+  double* out = G + static_cast<int64_t>(seg_slot[seg]) * C::P * 64;
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) {
+    const int p = warp + q * W;
+    if (q < C::Q - 1 || p < C::P)
+      *reinterpret_cast<double2*>(out + p * 64 + lane * 2) = make_double2(acc[q][0], acc[q][1]);
+  }
+}
+
+struct SolveArgs {
+  int row0;     // first local row of the batch
+  int nrows;    // rows in the batch
+  const int* row_slot0;
+  const int* row_nslot;
+  const double* G;
+};
+
+template <int NB>
+struct SolveCfg {
+  static constexpr int P = NB * (NB + 1) / 2;
+  static constexpr int PER_WARP = P * 64 + 2 * NB * 8;  // doubles: blocks + dinv + w
+  static constexpr int FIT = (220 * 1024) / (PER_WARP * 8);
+  static constexpr int WPB = FIT >= 8 ? 8 : (FIT < 1 ? 1 : FIT);
+};
+
+__device__ __forceinline__ int pidx(int I, int J) { return I * (I + 1) / 2 + J; }
+// Swizzled 8x8 block storage: element (r, c) at 8r + (c ^ 4*((r>>1)&1)); the
+// C-fragment (16-byte) and A/B-fragment (8-byte) accesses are conflict-free.
+__device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r >> 1) & 1))); }
+
+// K3: batched solve.  One warp per column: sums the column's partial Grams
+// (slot order), adds lambda*n_c, then a right-looking blocked LDL^T on the
+// augmented matrix (8-column panels factored in registers with shuffles,
+// trailing updates on the FP64 tensor cores), then back substitution.
+template <int NB>
+__global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
+    k_hs_solve(HsArgs a, SolveArgs s) {
+  using C = SolveCfg<NB>;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rl = blockIdx.x * C::WPB + warp;
+  if (rl >= s.nrows) return;
+  const int lr = s.row0 + rl;
+  const int n_f = a.n_f, ld = a.ld;
+  double* M = smem + static_cast<size_t>(warp) * C::PER_WARP;
+  double* dinv = M + C::P * 64;
+  double* w = dinv + NB * 8;
+  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
+  if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
+    for (int k = lane; k < ld; k += 32) out[k] = 0.0;
+    return;
+  }
+  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
+  if (!(shift > 0.0)) {
+    if (lane == 0) {
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  const int r = lane >> 2, q = lane & 3;
+  {
+    const int ns = s.row_nslot[lr];
+    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
+    int I = 0, J = 0;
+    for (int p = 0; p < C::P; ++p) {
+      double2 v = *reinterpret_cast<const double2*>(base + p * 64);
+      for (int t = 1; t < ns; ++t) {  // slot order -> deterministic
+        const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
+        v.x += u.x;
+        v.y += u.y;
+      }
+      if (I == J && 8 * I + r < n_f) {
+        if (2 * q == r) v.x += shift;
+        if (2 * q + 1 == r) v.y += shift;
+      }
+      *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
+      if (++J > I) {
+        ++I;
+        J = 0;
+      }
+    }
+  }
+  __syncwarp();
+  const int KP = (n_f + 7) / 8;
+  bool ok = true;
+  for (int K = 0; K < KP && ok; ++K) {
+    double pv[NB][2];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (K + i < NB) {
+        const double2 v = *reinterpret_cast<const double2*>(M + pidx(K + i, K) * 64 + swz(r, 2 * q));
+        pv[i][0] = v.x;
+        pv[i][1] = v.y;
+      }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int k = 8 * K + c;
+      if (k >= n_f) break;
+      const double d = __shfl_sync(kFull, pv[0][c & 1], 4 * c + (c >> 1));
+      if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
+        ok = false;
+        break;
+      }
+      const double inv = 1.0 / d;
+      if (lane == 0) dinv[k] = inv;
+      const double cv0 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + (c >> 1)) * inv;
+      const double cv1 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + 4 + (c >> 1)) * inv;
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (K + i < NB) {
+          const double aik = __shfl_sync(kFull, pv[i][c & 1], 4 * r + (c >> 1));
+          if (2 * q > c) pv[i][0] = fma(-aik, cv0, pv[i][0]);
+          if (2 * q + 1 > c) pv[i][1] = fma(-aik, cv1, pv[i][1]);
+        }
+    }
+    if (!ok) break;
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (K + i < NB)
+        *reinterpret_cast<double2*>(M + pidx(K + i, K) * 64 + swz(r, 2 * q)) =
+            make_double2(pv[i][0], pv[i][1]);
+    if (lane < 8 && 8 * K + lane >= n_f) dinv[8 * K + lane] = 0.0;  // non-pivot columns
+    __syncwarp();
+    if (K + 1 < KP) {
+      const double dk0 = dinv[8 * K + q], dk1 = dinv[8 * K + 4 + q];
+      double af[NB][2];
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (K + i < NB) {
+          const double* blk = M + pidx(K + i, K) * 64;
+          af[i][0] = -blk[swz(r, q)];
+          af[i][1] = -blk[swz(r, 4 + q)];
+        }
+      for (int J = K + 1; J < KP; ++J) {
+        const double* bj = M + pidx(J, K) * 64;
+        const double b0 = bj[swz(r, q)] * dk0, b1 = bj[swz(r, 4 + q)] * dk1;
+#pragma unroll
+        for (int i = 1; i < NB; ++i) {
+          const int I = K + i;
+          if (I >= J && I < NB) {
+            double* cb = M + pidx(I, J) * 64 + swz(r, 2 * q);
+            double2 cv = *reinterpret_cast<double2*>(cb);
+            dmma884(cv.x, cv.y, af[i][0], b0);
+            dmma884(cv.x, cv.y, af[i][1], b1);
+            *reinterpret_cast<double2*>(cb) = cv;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (!ok) {
+    if (lane == 0) {
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  // Back substitution: u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
+  const int IR = ld >> 3, rr = ld & 7;
+  for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
+  __syncwarp();
+  for (int k = n_f - 1; k >= 0; --k) {
+    const double u = w[k] * dinv[k];
+    const double* rowk = M + pidx(k >> 3, 0) * 64;
+    const int rk = k & 7;
+    for (int i = lane; i < k; i += 32) w[i] = fma(-rowk[(i >> 3) * 64 + swz(rk, i & 7)], u, w[i]);
+    __syncwarp();
+    if (lane == 0) w[k] = u;
+    __syncwarp();
+  }
+  for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
+}
+
 // ------------------------------------------------------------ fallback --
 // Least-norm solve for listed rows.  Workspace per CTA: W (n x n), Q (n x n).
 constexpr int kFbThreads = 256;
@@ -501,35 +699,78 @@ __global__ void __launch_bounds__(kFbThreads) k_hs_fallback(HsArgs a, double* wo
 
 template <int NB>
 struct Mode {
-  static constexpr int GW = NB <= 4 ? 1 : (NB <= 16 ? 4 : 8);
+  static constexpr int GW = NB <= 4 ? 1 : (NB <= 16 ? 4 : (NB <= 20 ? 8 : 16));
 };
 
+constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
+
 template <int NB>
-void run_hs(Ctx* ctx, HsArgs& a, const SegPlan& P) {
+void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
   constexpr int GW = Mode<NB>::GW;
   using C = HsCfg<NB, GW>;
-  const size_t smem = sizeof(double) * hs_group_doubles<NB, GW>(a.ld) * C::GPC;
-  static bool attr_set = false;
-  if (!attr_set) {
-    AB2_CUDA(cudaFuncSetAttribute(k_hs_main<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    AB2_CUDA(cudaFuncSetAttribute(k_hs_reduce<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    attr_set = true;
-  }
-  if (P.n_slots > 0)
-    a.partial = static_cast<double*>(ctx->scratch(2, sizeof(double) * C::PART * P.n_slots));
-  {
-    const int blocks = (P.n_seg + C::GPC - 1) / C::GPC;
-    const int tok = ctx->begin_launch("halfsweep_gram_solve");
-    k_hs_main<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
-    ctx->end_launch(tok);
-  }
-  if (P.n_multi > 0) {
-    const int blocks = (P.n_multi + C::GPC - 1) / C::GPC;
-    const int tok = ctx->begin_launch("halfsweep_reduce_solve");
-    k_hs_reduce<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
-    ctx->end_launch(tok);
+  if constexpr (NB <= 4) {
+    // fused warp-per-segment kernel (Gram + solve in one pass)
+    const SegPlan& P = R.plan(kind, S);
+    a.seg_row = P.seg_row;
+    a.seg_beg = P.seg_beg;
+    a.seg_len = P.seg_len;
+    a.seg_slot = P.seg_slot;
+    a.n_seg = P.n_seg;
+    a.m_row = P.m_row;
+    a.m_slot0 = P.m_slot0;
+    a.m_nslot = P.m_nslot;
+    a.n_multi = P.n_multi;
+    const size_t smem = sizeof(double) * hs_group_doubles<NB, GW>(a.ld) * C::GPC;
+    static bool attr_set = false;
+    if (!attr_set) {
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_main<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_reduce<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr_set = true;
+    }
+    if (P.n_slots > 0)
+      a.partial = static_cast<double*>(ctx->scratch(2, sizeof(double) * C::PART * P.n_slots));
+    {
+      const int blocks = (P.n_seg + C::GPC - 1) / C::GPC;
+      const int tok = ctx->begin_launch("halfsweep_fused");
+      k_hs_main<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
+      ctx->end_launch(tok);
+    }
+    if (P.n_multi > 0) {
+      const int blocks = (P.n_multi + C::GPC - 1) / C::GPC;
+      const int tok = ctx->begin_launch("halfsweep_fused_reduce");
+      k_hs_reduce<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
+      ctx->end_launch(tok);
+    }
+  } else {
+    using SC = SolveCfg<NB>;
+    const size_t slot_bytes = sizeof(double) * C::P * 64;
+    const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
+    const size_t gsmem = sizeof(double) * 2 * C::CH * C::LDS;
+    const size_t ssmem = sizeof(double) * SC::PER_WARP * SC::WPB;
+    static bool attr_set = false;
+    if (!attr_set) {
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr_set = true;
+    }
+    double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
+    for (const HsBatch& b : P.batches) {
+      if (b.seg1 > b.seg0) {
+        const int tok = ctx->begin_launch("halfsweep_gram");
+        k_hs_gram<NB, GW><<<b.seg1 - b.seg0, GW * 32, gsmem, ctx->stream>>>(
+            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
+        ctx->end_launch(tok);
+      }
+      SolveArgs s;
+      s.row0 = b.row0;
+      s.nrows = b.row1 - b.row0;
+      s.row_slot0 = P.row_slot0;
+      s.row_nslot = P.row_nslot;
+      s.G = G;
+      const int tok = ctx->begin_launch("halfsweep_solve");
+      k_hs_solve<NB><<<(s.nrows + SC::WPB - 1) / SC::WPB, SC::WPB * 32, ssmem, ctx->stream>>>(a, s);
+      ctx->end_launch(tok);
+    }
   }
 }
 
@@ -548,7 +789,6 @@ void launch_half_sweep(DevRatings& R, int kind, int n_f, const double* src_rows,
   const View& v = R.view(kind);
   if (v.nrows == 0) return;
   const int ld = row_stride(n_f);
-  const SegPlan& P = R.plan(kind, hs_segment_size(n_f));
   HsArgs a;
   a.ptr = v.ptr;
   a.idx = v.idx;
@@ -559,15 +799,6 @@ void launch_half_sweep(DevRatings& R, int kind, int n_f, const double* src_rows,
   a.n_f = n_f;
   a.ld = ld;
   a.lambda = lambda;
-  a.seg_row = P.seg_row;
-  a.seg_beg = P.seg_beg;
-  a.seg_len = P.seg_len;
-  a.seg_slot = P.seg_slot;
-  a.n_seg = P.n_seg;
-  a.m_row = P.m_row;
-  a.m_slot0 = P.m_slot0;
-  a.m_nslot = P.m_nslot;
-  a.n_multi = P.n_multi;
   a.partial = nullptr;
   // fallback bookkeeping: counters[2+...] region
   unsigned* fb_count = ctx->d_counters + 8;
@@ -578,7 +809,7 @@ void launch_half_sweep(DevRatings& R, int kind, int n_f, const double* src_rows,
   switch (gram_blocks(n_f)) {
 #define AB2_HS_CASE(NB) \
   case NB:              \
-    run_hs<NB>(ctx, a, P); \
+    run_hs<NB>(ctx, R, kind, a, hs_segment_size(n_f)); \
     break;
     AB2_HS_CASE(1) AB2_HS_CASE(2) AB2_HS_CASE(3) AB2_HS_CASE(4) AB2_HS_CASE(5) AB2_HS_CASE(6)
     AB2_HS_CASE(7) AB2_HS_CASE(8) AB2_HS_CASE(9) AB2_HS_CASE(10) AB2_HS_CASE(11) AB2_HS_CASE(12)

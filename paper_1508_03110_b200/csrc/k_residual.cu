@@ -82,19 +82,34 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_gradient(GradArgs a) {
   double2 acc[V2];
 #pragma unroll
   for (int k = 0; k < V2; ++k) acc[k] = make_double2(0.0, 0.0);
-  for (int t0 = 0; t0 < len; t0 += R) {
-    const int t = t0 + sg;
-    const bool ok = t < len;
-    const int j = ok ? a.idx[beg + t] : 0;
-    const double r = ok ? a.val[beg + t] : 0.0;
-    double2 m[V2];
-    load_row<TPR, V2>(a.xother + static_cast<int64_t>(j) * ld, ld, sl, m);
-    const double s = group_sum<TPR>(dot2<V2>(xu, m));
-    const double e2 = ok ? 2.0 * (s - r) : 0.0;
+  // two ratings per sub-group per trip: both gathers are in flight together
+  for (int t0 = 0; t0 < len; t0 += 2 * R) {
+    int j[2];
+    double r[2];
+    bool ok[2];
 #pragma unroll
-    for (int k = 0; k < V2; ++k) {
-      acc[k].x = fma(e2, m[k].x, acc[k].x);
-      acc[k].y = fma(e2, m[k].y, acc[k].y);
+    for (int u = 0; u < 2; ++u) {
+      const int t = t0 + sg + u * R;
+      ok[u] = t < len;
+      j[u] = ok[u] ? a.idx[beg + t] : 0;
+      r[u] = ok[u] ? a.val[beg + t] : 0.0;
+    }
+    double2 m[2][V2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) load_row<TPR, V2>(a.xother + static_cast<int64_t>(j[u]) * ld, ld, sl, m[u]);
+    double s[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) s[u] = dot2<V2>(xu, m[u]);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) s[u] = group_sum<TPR>(s[u]);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double e2 = ok[u] ? 2.0 * (s[u] - r[u]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < V2; ++k) {
+        acc[k].x = fma(e2, m[u][k].x, acc[k].x);
+        acc[k].y = fma(e2, m[u][k].y, acc[k].y);
+      }
     }
   }
 #pragma unroll
@@ -205,34 +220,63 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_quartic(QuartArgs a) {
           if (lane == 0) dd_add(acc[1], static_cast<double>(count) * xx);
         }
       }
-      for (int64_t t0 = b; t0 < e; t0 += R) {
-        const int64_t t = t0 + sg;
-        const bool ok = t < e;
-        const int j = ok ? a.uidx[t] : 0;
-        const double r = ok ? a.uval[t] : 0.0;
-        const int64_t mrow = static_cast<int64_t>(a.n_u + j) * ld;
-        double2 xm[V2];
-        load_row<TPR, V2>(a.x + mrow, ld, sl, xm);
+      for (int64_t t0 = b; t0 < e; t0 += 2 * R) {
+        int j[2];
+        double r[2];
+        bool ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t t = t0 + sg + u * R;
+          ok[u] = t < e;
+          j[u] = ok[u] ? a.uidx[t] : 0;
+          r[u] = ok[u] ? a.uval[t] : 0.0;
+        }
+        double2 xm[2][V2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          load_row<TPR, V2>(a.x + static_cast<int64_t>(a.n_u + j[u]) * ld, ld, sl, xm[u]);
         if constexpr (QUART) {
-          double2 pm[V2];
-          load_row<TPR, V2>(a.p + mrow, ld, sl, pm);
-          const double sa = group_sum<TPR>(dot2<V2>(xu, xm));
-          const double sb = group_sum<TPR>(dot2<V2>(xu, pm) + dot2<V2>(pu, xm));
-          const double sd = group_sum<TPR>(dot2<V2>(pu, pm));
-          if (ok && sl == 0) {
-            // residual along the step: a - b*alpha - d*alpha^2 (linesearch.cpp:76-88)
-            const double ra = r - sa;
-            dd_add(acc[0], ra * ra);
-            dd_add(acc[1], -2.0 * ra * sb);
-            dd_add(acc[2], sb * sb - 2.0 * ra * sd);
-            dd_add(acc[3], 2.0 * sb * sd);
-            dd_add(acc[4], sd * sd);
+          double2 pm[2][V2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            load_row<TPR, V2>(a.p + static_cast<int64_t>(a.n_u + j[u]) * ld, ld, sl, pm[u]);
+          double sa[2], sb[2], sd[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            sa[u] = dot2<V2>(xu, xm[u]);
+            sb[u] = dot2<V2>(xu, pm[u]) + dot2<V2>(pu, xm[u]);
+            sd[u] = dot2<V2>(pu, pm[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            sa[u] = group_sum<TPR>(sa[u]);
+            sb[u] = group_sum<TPR>(sb[u]);
+            sd[u] = group_sum<TPR>(sd[u]);
+          }
+          if (sl == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (!ok[u]) continue;
+              // residual along the step: a - b*alpha - d*alpha^2 (linesearch.cpp:76-88)
+              const double ra = r[u] - sa[u];
+              dd_add(acc[0], ra * ra);
+              dd_add(acc[1], -2.0 * ra * sb[u]);
+              dd_add(acc[2], sb[u] * sb[u] - 2.0 * ra * sd[u]);
+              dd_add(acc[3], 2.0 * sb[u] * sd[u]);
+              dd_add(acc[4], sd[u] * sd[u]);
+            }
           }
         } else {
-          const double sa = group_sum<TPR>(dot2<V2>(xu, xm));
-          if (ok && sl == 0) {
-            const double ra = r - sa;
-            dd_add(acc[0], ra * ra);
+          double sa[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) sa[u] = group_sum<TPR>(dot2<V2>(xu, xm[u]));
+          if (sl == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (!ok[u]) continue;
+              const double ra = r[u] - sa[u];
+              dd_add(acc[0], ra * ra);
+            }
           }
         }
       }
@@ -299,30 +343,32 @@ struct Geometry {
 };
 
 Geometry geometry_for(int n_f) {
+  // TPR lanes per rating, V2 <= 4 double2 per lane: few shuffle rounds and
+  // 32/TPR ratings in flight per warp step.
   const int pairs = row_stride(n_f) / 2;  // double2 per row
-  if (pairs <= 1) return {1, 1};
-  if (pairs <= 2) return {2, 1};
-  if (pairs <= 4) return {4, 1};
-  if (pairs <= 8) return {8, 1};
-  if (pairs <= 16) return {16, 1};
-  if (pairs <= 32) return {32, 1};
-  if (pairs <= 64) return {32, 2};
-  if (pairs <= 96) return {32, 3};
-  if (pairs <= 128) return {32, 4};
-  throw Error(ALSNCG_EUNSUPPORTED, "n_f too large for the residual kernels");
+  int tpr = 1;
+  while (tpr * 4 < pairs) tpr *= 2;
+  if (tpr > 32) throw Error(ALSNCG_EUNSUPPORTED, "n_f too large for the residual kernels");
+  const int v2 = (pairs + tpr - 1) / tpr;
+  return {tpr, v2};
 }
 
-#define AB2_GEOM_DISPATCH(G, MACRO)                              \
-  do {                                                           \
-    if (G.tpr == 1) { MACRO(1, 1); }                             \
-    else if (G.tpr == 2) { MACRO(2, 1); }                        \
-    else if (G.tpr == 4) { MACRO(4, 1); }                        \
-    else if (G.tpr == 8) { MACRO(8, 1); }                        \
-    else if (G.tpr == 16) { MACRO(16, 1); }                      \
-    else if (G.v2 == 1) { MACRO(32, 1); }                        \
-    else if (G.v2 == 2) { MACRO(32, 2); }                        \
-    else if (G.v2 == 3) { MACRO(32, 3); }                        \
-    else { MACRO(32, 4); }                                       \
+#define AB2_GEOM_V(T, G, MACRO)          \
+  do {                                   \
+    if (G.v2 == 1) { MACRO(T, 1); }      \
+    else if (G.v2 == 2) { MACRO(T, 2); } \
+    else if (G.v2 == 3) { MACRO(T, 3); } \
+    else { MACRO(T, 4); }                \
+  } while (0)
+
+#define AB2_GEOM_DISPATCH(G, MACRO)                      \
+  do {                                                   \
+    if (G.tpr == 1) { AB2_GEOM_V(1, G, MACRO); }         \
+    else if (G.tpr == 2) { AB2_GEOM_V(2, G, MACRO); }    \
+    else if (G.tpr == 4) { AB2_GEOM_V(4, G, MACRO); }    \
+    else if (G.tpr == 8) { AB2_GEOM_V(8, G, MACRO); }    \
+    else if (G.tpr == 16) { AB2_GEOM_V(16, G, MACRO); }  \
+    else { AB2_GEOM_V(32, G, MACRO); }                   \
   } while (0)
 
 constexpr int kGradSeg = 2048;
