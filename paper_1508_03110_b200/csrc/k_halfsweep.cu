@@ -415,24 +415,26 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
   {
     const int ns = s.row_nslot[lr];
     const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
-    int I = 0, J = 0;
-    for (int p = 0; p < C::P; ++p) {
-      double2 v = *reinterpret_cast<const double2*>(base + p * 64);
-      for (int t = 1; t < ns; ++t) {  // slot order -> deterministic
-        const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
-        v.x += u.x;
-        v.y += u.y;
-      }
-      if (I == J && 8 * I + r < n_f) {
-        if (2 * q == r) v.x += shift;
-        if (2 * q + 1 == r) v.y += shift;
-      }
-      *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
-      if (++J > I) {
-        ++I;
-        J = 0;
+    if (ns == 1) {
+      // one slot: bulk 16-byte async copies straight into the swizzled blocks
+      for (int p = 0; p < C::P; ++p) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
+      cp_async_commit();
+      cp_async_wait<0>();
+    } else {
+      for (int p = 0; p < C::P; ++p) {  // heavy rows: sum slots in slot order
+        double2 v = *reinterpret_cast<const double2*>(base + p * 64);
+        for (int t = 1; t < ns; ++t) {
+          const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
+          v.x += u.x;
+          v.y += u.y;
+        }
+        *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
       }
     }
+    __syncwarp();
+    // lambda * n_c on the diagonal (als.cpp:58-59): lane (r, q) owns (r, 2q+e)
+    for (int I = 0; I < NB; ++I)
+      if (8 * I + r < n_f && (r >> 1) == q) M[pidx(I, I) * 64 + swz(r, r)] += shift;
   }
   __syncwarp();
   const int KP = (n_f + 7) / 8;
@@ -510,17 +512,34 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
     }
     return;
   }
-  // Back substitution: u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
+  // Back substitution: u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k, one
+  // 8-row panel at a time: the panel's 8 unknowns by shuffles in lanes 0..7,
+  // then every lane folds them into the remaining right-hand side.
   const int IR = ld >> 3, rr = ld & 7;
   for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
   __syncwarp();
-  for (int k = n_f - 1; k >= 0; --k) {
-    const double u = w[k] * dinv[k];
-    const double* rowk = M + pidx(k >> 3, 0) * 64;
-    const int rk = k & 7;
-    for (int i = lane; i < k; i += 32) w[i] = fma(-rowk[(i >> 3) * 64 + swz(rk, i & 7)], u, w[i]);
-    __syncwarp();
-    if (lane == 0) w[k] = u;
+  for (int K = KP - 1; K >= 0; --K) {
+    const int kc = 8 * K + (lane & 7);
+    double wk = (lane < 8 && kc < n_f) ? w[kc] : 0.0;
+    const double dk = (lane < 8 && kc < n_f) ? dinv[kc] : 0.0;
+#pragma unroll
+    for (int c = 7; c >= 0; --c) {
+      const double u = __shfl_sync(kFull, wk * dk, c);
+      if (lane < c) wk = fma(-M[pidx(K, K) * 64 + swz(c, lane)], u, wk);
+      if (lane == c) wk = u;
+    }
+    if (lane < 8 && kc < n_f) w[kc] = wk;
+    double uu[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) uu[c] = __shfl_sync(kFull, wk, c);
+    for (int i = lane; i < 8 * K; i += 32) {
+      const double* blk = M + pidx(K, i >> 3) * 64;
+      double acc = w[i];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (8 * K + c < n_f) acc = fma(-blk[swz(c, i & 7)], uu[c], acc);
+      w[i] = acc;
+    }
     __syncwarp();
   }
   for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;

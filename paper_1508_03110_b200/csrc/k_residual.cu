@@ -197,87 +197,81 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_quartic(QuartArgs a) {
   const int lo = tile * kTileRows;
   if (user_tile) {
     const int hi = min(lo + kTileRows, a.nurows);
+    // per-row regularisation (linesearch.cpp:68-73; ncg.cpp:57-61)
     for (int lr = lo + warp; lr < hi; lr += kWarpsPerBlock) {
-      const int64_t b = a.uptr[lr], e = a.uptr[lr + 1];
-      const int count = static_cast<int>(e - b);
+      const int count = static_cast<int>(a.uptr[lr + 1] - a.uptr[lr]);
       const int64_t urow = static_cast<int64_t>(a.urow0 + lr) * ld;
       double2 xu[V2], pu[V2];
       load_row<TPR, V2>(a.x + urow, ld, sl, xu);
-      if constexpr (QUART) load_row<TPR, V2>(a.p + urow, ld, sl, pu);
-      // per-row regularisation (linesearch.cpp:68-73; ncg.cpp:57-61)
-      {
-        const double xx = group_sum<TPR>(dot2<V2>(xu, xu));
-        if constexpr (QUART) {
-          const double xp = group_sum<TPR>(dot2<V2>(xu, pu));
-          const double pp = group_sum<TPR>(dot2<V2>(pu, pu));
-          if (lane == 0 && a.lambda > 0.0 && count > 0) {
-            const double w = a.lambda * count;
-            dd_add(acc[0], w * xx);
-            dd_add(acc[1], 2.0 * w * xp);
-            dd_add(acc[2], w * pp);
-          }
-        } else {
-          if (lane == 0) dd_add(acc[1], static_cast<double>(count) * xx);
+      const double xx = group_sum<TPR>(dot2<V2>(xu, xu));
+      if constexpr (QUART) {
+        load_row<TPR, V2>(a.p + urow, ld, sl, pu);
+        const double xp = group_sum<TPR>(dot2<V2>(xu, pu));
+        const double pp = group_sum<TPR>(dot2<V2>(pu, pu));
+        if (lane == 0 && a.lambda > 0.0 && count > 0) {
+          const double w = a.lambda * count;
+          dd_add(acc[0], w * xx);
+          dd_add(acc[1], 2.0 * w * xp);
+          dd_add(acc[2], w * pp);
         }
+      } else {
+        if (lane == 0) dd_add(acc[1], static_cast<double>(count) * xx);
       }
-      for (int64_t t0 = b; t0 < e; t0 += 2 * R) {
-        int j[2];
-        double r[2];
-        bool ok[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int64_t t = t0 + sg + u * R;
-          ok[u] = t < e;
-          j[u] = ok[u] ? a.uidx[t] : 0;
-          r[u] = ok[u] ? a.uval[t] : 0.0;
+    }
+    // Ratings of the tile split evenly over the CTA's sub-groups (contiguous
+    // chunks; a sub-group walks the users its chunk crosses), so a heavy user
+    // no longer idles the other warps of its tile.
+    constexpr int NG = kWarpsPerBlock * R;
+    const int64_t T0 = a.uptr[lo], T1 = a.uptr[hi];
+    const int64_t chunk = (T1 - T0 + NG - 1) / NG;
+    int64_t t = T0 + static_cast<int64_t>(warp * R + sg) * chunk;
+    const int64_t tend = min(T1, t + chunk);
+    int u = lo, uhi = hi;
+    if (t < tend) {
+      while (uhi - u > 1) {
+        const int mid = (u + uhi) >> 1;
+        if (a.uptr[mid] <= t) u = mid; else uhi = mid;
+      }
+    }
+    int64_t uend = t < tend ? a.uptr[u + 1] : 0;
+    double2 xu[V2], pu[V2];
+    load_row<TPR, V2>(a.x + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, xu);
+    if constexpr (QUART) load_row<TPR, V2>(a.p + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, pu);
+    for (int64_t s = 0; s < chunk; ++s, ++t) {
+      const bool ok = t < tend;
+      if (ok && t >= uend) {
+        do {
+          ++u;
+          uend = a.uptr[u + 1];
+        } while (t >= uend);
+        load_row<TPR, V2>(a.x + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, xu);
+        if constexpr (QUART) load_row<TPR, V2>(a.p + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, pu);
+      }
+      const int j = ok ? a.uidx[t] : 0;
+      const double r = ok ? a.uval[t] : 0.0;
+      const int64_t mrow = static_cast<int64_t>(a.n_u + j) * ld;
+      double2 xm[V2];
+      load_row<TPR, V2>(a.x + mrow, ld, sl, xm);
+      if constexpr (QUART) {
+        double2 pm[V2];
+        load_row<TPR, V2>(a.p + mrow, ld, sl, pm);
+        const double sa = group_sum<TPR>(dot2<V2>(xu, xm));
+        const double sb = group_sum<TPR>(dot2<V2>(xu, pm) + dot2<V2>(pu, xm));
+        const double sd = group_sum<TPR>(dot2<V2>(pu, pm));
+        if (ok && sl == 0) {
+          // residual along the step: a - b*alpha - d*alpha^2 (linesearch.cpp:76-88)
+          const double ra = r - sa;
+          dd_add(acc[0], ra * ra);
+          dd_add(acc[1], -2.0 * ra * sb);
+          dd_add(acc[2], sb * sb - 2.0 * ra * sd);
+          dd_add(acc[3], 2.0 * sb * sd);
+          dd_add(acc[4], sd * sd);
         }
-        double2 xm[2][V2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          load_row<TPR, V2>(a.x + static_cast<int64_t>(a.n_u + j[u]) * ld, ld, sl, xm[u]);
-        if constexpr (QUART) {
-          double2 pm[2][V2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            load_row<TPR, V2>(a.p + static_cast<int64_t>(a.n_u + j[u]) * ld, ld, sl, pm[u]);
-          double sa[2], sb[2], sd[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            sa[u] = dot2<V2>(xu, xm[u]);
-            sb[u] = dot2<V2>(xu, pm[u]) + dot2<V2>(pu, xm[u]);
-            sd[u] = dot2<V2>(pu, pm[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            sa[u] = group_sum<TPR>(sa[u]);
-            sb[u] = group_sum<TPR>(sb[u]);
-            sd[u] = group_sum<TPR>(sd[u]);
-          }
-          if (sl == 0) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              if (!ok[u]) continue;
-              // residual along the step: a - b*alpha - d*alpha^2 (linesearch.cpp:76-88)
-              const double ra = r[u] - sa[u];
-              dd_add(acc[0], ra * ra);
-              dd_add(acc[1], -2.0 * ra * sb[u]);
-              dd_add(acc[2], sb[u] * sb[u] - 2.0 * ra * sd[u]);
-              dd_add(acc[3], 2.0 * sb[u] * sd[u]);
-              dd_add(acc[4], sd[u] * sd[u]);
-            }
-          }
-        } else {
-          double sa[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) sa[u] = group_sum<TPR>(dot2<V2>(xu, xm[u]));
-          if (sl == 0) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              if (!ok[u]) continue;
-              const double ra = r[u] - sa[u];
-              dd_add(acc[0], ra * ra);
-            }
-          }
+      } else {
+        const double sa = group_sum<TPR>(dot2<V2>(xu, xm));
+        if (ok && sl == 0) {
+          const double ra = r - sa;
+          dd_add(acc[0], ra * ra);
         }
       }
     }
