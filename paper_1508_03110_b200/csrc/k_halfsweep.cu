@@ -30,6 +30,10 @@ namespace ab2 {
 
 namespace {
 
+// One dynamic shared-memory array for every kernel of this file; all shared
+// accesses index it with 32-bit offsets so they compile to LDS/STS.
+extern __shared__ __align__(16) double g_smem[];
+
 struct HsArgs {
   const int64_t* ptr;
   const int* idx;
@@ -105,28 +109,28 @@ __device__ __forceinline__ void pair_ij(int p, int& I, int& J) {
 }
 
 // Gram of the augmented rows over one segment, accumulated into acc.
+// sb: offset (in doubles) of the group's region in g_smem.
 template <int NB, int GW>
-__device__ __forceinline__ void gram_segment(const HsArgs& a, double* S, int64_t beg, int len,
+__device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t beg, int len,
                                              int gtid, int warp, int lane,
                                              double (&acc)[HsCfg<NB, GW>::Q][2],
                                              const int (&pI)[HsCfg<NB, GW>::Q],
                                              const int (&pJ)[HsCfg<NB, GW>::Q]) {
   using C = HsCfg<NB, GW>;
+  constexpr int BUF = C::CH * C::LDS;
   const int ld = a.ld;
   const int nch = ld >> 1;  // 16-byte chunks per source row
-  double* buf[2] = {S, S + C::CH * C::LDS};
-  // zero the pad columns (ld, ld+1 .. NB*8) once; column ld carries r
-  for (int e = gtid; e < 2 * C::CH * (C::LDS - ld); e += C::GT) {
-    const int b = e / (C::CH * (C::LDS - ld));
-    const int rem = e % (C::CH * (C::LDS - ld));
-    const int t = rem / (C::LDS - ld), c = rem % (C::LDS - ld);
-    buf[b][t * C::LDS + ld + c] = 0.0;
+  const int padw = C::LDS - ld;
+  // zero the pad columns (ld .. LDS) of both buffers once; column ld carries r
+  for (int e = gtid; e < 2 * C::CH * padw; e += C::GT) {
+    const int t = e / padw, c = e - t * padw;  // t indexes rows of both buffers
+    g_smem[sb + t * C::LDS + ld + c] = 0.0;
   }
   group_sync<GW>();
   // Each warp loads the stage's CH indices with one coalesced load (lane t
   // holds rating t) and hands them out by shuffle, so every cp.async of the
   // stage issues after a single index-load latency.
-  auto issue = [&](int s, double* B) {
+  auto issue = [&](int s, int bo) {
     const int base = s * C::CH;
     const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
     for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
@@ -134,7 +138,7 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, double* S, int64_t
       const int t = min(c / nch, C::CH - 1), k = c - t * nch;
       const int j = __shfl_sync(kFull, jv, t);
       if (c < C::CH * nch) {
-        double* dst = B + t * C::LDS + 2 * k;
+        double* dst = &g_smem[bo + t * C::LDS + 2 * k];
         if (base + t < len)
           cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
         else
@@ -143,30 +147,37 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, double* S, int64_t
     }
     for (int t = gtid; t < C::CH; t += C::GT) {
       const int rt = base + t;
-      B[t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
+      g_smem[bo + t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
     }
   };
+  int aoff[C::Q], boff[C::Q];
+#pragma unroll
+  for (int q = 0; q < C::Q; ++q) {
+    aoff[q] = 8 * pI[q];
+    boff[q] = 8 * pJ[q];
+  }
+  const int lofs = (lane & 3) * C::LDS + (lane >> 2);
   const int nst = (len + C::CH - 1) / C::CH;
-  if (nst > 0) issue(0, buf[0]);
+  if (nst > 0) issue(0, sb);
   cp_async_commit();
   for (int s = 0; s < nst; ++s) {
     if (s + 1 < nst) {
-      issue(s + 1, buf[(s + 1) & 1]);
+      issue(s + 1, sb + ((s + 1) & 1) * BUF);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     group_sync<GW>();
-    const double* B = buf[s & 1];
+    const int bo = sb + (s & 1) * BUF + lofs;
 #pragma unroll 2
     for (int kk = 0; kk < C::CH / 4; ++kk) {
-      const double* base = B + (kk * 4 + (lane & 3)) * C::LDS + (lane >> 2);
+      const int base = bo + kk * 4 * C::LDS;
 #pragma unroll
       for (int q = 0; q < C::Q; ++q) {
         if (q < C::Q - 1 || warp + q * GW < C::P) {
-          const double av = base[8 * pI[q]];
-          const double bv = base[8 * pJ[q]];
+          const double av = g_smem[base + aoff[q]];
+          const double bv = g_smem[base + boff[q]];
           dmma884(acc[q][0], acc[q][1], av, bv);
         }
       }
@@ -275,13 +286,13 @@ __device__ __forceinline__ void init_pairs(int warp, int (&pI)[HsCfg<NB, GW>::Q]
 template <int NB, int GW>
 __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
   using C = HsCfg<NB, GW>;
-  extern __shared__ __align__(16) double smem[];
   const int group = threadIdx.x / C::GT;
   const int gtid = threadIdx.x % C::GT;
   const int warp = gtid >> 5, lane = gtid & 31;
   const int seg = blockIdx.x * C::GPC + group;
   if (seg >= a.n_seg) return;  // uniform per group (GW==1 groups are warps)
-  double* S = smem + static_cast<size_t>(group) * hs_group_doubles<NB, GW>(a.ld);
+  const int sbase = group * static_cast<int>(hs_group_doubles<NB, GW>(a.ld));
+  double* S = g_smem + sbase;
   const int lr = a.seg_row[seg];
   const int len = a.seg_len[seg];
   const int slot = a.seg_slot[seg];
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
   int pI[C::Q], pJ[C::Q];
   double acc[C::Q][2];
   init_pairs<NB, GW>(warp, pI, pJ, acc);
-  gram_segment<NB, GW>(a, S, a.seg_beg[seg], len, gtid, warp, lane, acc, pI, pJ);
+  gram_segment<NB, GW>(a, sbase, a.seg_beg[seg], len, gtid, warp, lane, acc, pI, pJ);
   if (slot >= 0) {
     double* P = a.partial + static_cast<int64_t>(slot) * C::PART;
 #pragma unroll
@@ -308,13 +319,12 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
 template <int NB, int GW>
 __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) {
   using C = HsCfg<NB, GW>;
-  extern __shared__ __align__(16) double smem[];
   const int group = threadIdx.x / C::GT;
   const int gtid = threadIdx.x % C::GT;
   const int warp = gtid >> 5, lane = gtid & 31;
   const int m = blockIdx.x * C::GPC + group;
   if (m >= a.n_multi) return;
-  double* S = smem + static_cast<size_t>(group) * hs_group_doubles<NB, GW>(a.ld);
+  double* S = g_smem + static_cast<size_t>(group) * hs_group_doubles<NB, GW>(a.ld);
   int pI[C::Q], pJ[C::Q];
   double acc[C::Q][2];
   init_pairs<NB, GW>(warp, pI, pJ, acc);
@@ -343,13 +353,12 @@ __global__ void __launch_bounds__(W * 32) k_hs_gram(HsArgs a, const int* __restr
                                                     const int* __restrict__ seg_slot,
                                                     double* __restrict__ G) {
   using C = HsCfg<NB, W>;
-  extern __shared__ __align__(16) double smem[];
   const int gtid = threadIdx.x, warp = gtid >> 5, lane = gtid & 31;
   const int seg = blockIdx.x;
   int pI[C::Q], pJ[C::Q];
   double acc[C::Q][2];
   init_pairs<NB, W>(warp, pI, pJ, acc);
-  gram_segment<NB, W>(a, smem, seg_beg[seg], seg_len[seg], gtid, warp, lane, acc, pI, pJ);
+  gram_segment<NB, W>(a, 0, seg_beg[seg], seg_len[seg], gtid, warp, lane, acc, pI, pJ);
   double* out = G + static_cast<int64_t>(seg_slot[seg]) * C::P * 64;
 #pragma unroll
   for (int q = 0; q < C::Q; ++q) {
@@ -388,13 +397,12 @@ template <int NB>
 __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
     k_hs_solve(HsArgs a, SolveArgs s) {
   using C = SolveCfg<NB>;
-  extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rl = blockIdx.x * C::WPB + warp;
   if (rl >= s.nrows) return;
   const int lr = s.row0 + rl;
   const int n_f = a.n_f, ld = a.ld;
-  double* M = smem + static_cast<size_t>(warp) * C::PER_WARP;
+  double* M = g_smem + static_cast<size_t>(warp) * C::PER_WARP;
   double* dinv = M + C::P * 64;
   double* w = dinv + NB * 8;
   double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
