@@ -460,21 +460,26 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
     for (int c = 0; c < 8; ++c) {
       const int k = 8 * K + c;
       if (k >= n_f) break;
+      // all shuffles of the step first (none depends on the pivot), then 1/d
       const double d = __shfl_sync(kFull, pv[0][c & 1], 4 * c + (c >> 1));
+      const double cr0 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + (c >> 1));
+      const double cr1 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + 4 + (c >> 1));
+      double aik[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (K + i < NB) aik[i] = __shfl_sync(kFull, pv[i][c & 1], 4 * r + (c >> 1));
       if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
         ok = false;
         break;
       }
       const double inv = 1.0 / d;
       if (lane == 0) dinv[k] = inv;
-      const double cv0 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + (c >> 1)) * inv;
-      const double cv1 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + 4 + (c >> 1)) * inv;
+      const double cv0 = cr0 * inv, cv1 = cr1 * inv;
 #pragma unroll
       for (int i = 0; i < NB; ++i)
         if (K + i < NB) {
-          const double aik = __shfl_sync(kFull, pv[i][c & 1], 4 * r + (c >> 1));
-          if (2 * q > c) pv[i][0] = fma(-aik, cv0, pv[i][0]);
-          if (2 * q + 1 > c) pv[i][1] = fma(-aik, cv1, pv[i][1]);
+          if (2 * q > c) pv[i][0] = fma(-aik[i], cv0, pv[i][0]);
+          if (2 * q + 1 > c) pv[i][1] = fma(-aik[i], cv1, pv[i][1]);
         }
     }
     if (!ok) break;
@@ -498,17 +503,22 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
       for (int J = K + 1; J < KP; ++J) {
         const double* bj = M + pidx(J, K) * 64;
         const double b0 = bj[swz(r, q)] * dk0, b1 = bj[swz(r, 4 + q)] * dk1;
+        // explicit load -> MMA -> store phases so the block updates overlap
+        double2 cv[NB];
 #pragma unroll
-        for (int i = 1; i < NB; ++i) {
-          const int I = K + i;
-          if (I >= J && I < NB) {
-            double* cb = M + pidx(I, J) * 64 + swz(r, 2 * q);
-            double2 cv = *reinterpret_cast<double2*>(cb);
-            dmma884(cv.x, cv.y, af[i][0], b0);
-            dmma884(cv.x, cv.y, af[i][1], b1);
-            *reinterpret_cast<double2*>(cb) = cv;
-          }
-        }
+        for (int i = 1; i < NB; ++i)
+          if (K + i >= J && K + i < NB)
+            cv[i] = *reinterpret_cast<const double2*>(M + pidx(K + i, J) * 64 + swz(r, 2 * q));
+#pragma unroll
+        for (int i = 1; i < NB; ++i)
+          if (K + i >= J && K + i < NB) dmma884(cv[i].x, cv[i].y, af[i][0], b0);
+#pragma unroll
+        for (int i = 1; i < NB; ++i)
+          if (K + i >= J && K + i < NB) dmma884(cv[i].x, cv[i].y, af[i][1], b1);
+#pragma unroll
+        for (int i = 1; i < NB; ++i)
+          if (K + i >= J && K + i < NB)
+            *reinterpret_cast<double2*>(M + pidx(K + i, J) * 64 + swz(r, 2 * q)) = cv[i];
       }
     }
     __syncwarp();
