@@ -344,28 +344,167 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
 }
 
 // ------------------------------------------------ split path (n_f >= 31) --
-// K1/K2: Gram-only kernel.  One CTA of W warps per segment; the augmented
-// Gram of the segment is written as NB(NB+1)/2 canonical 8x8 blocks in
-// C-fragment order (lane-major, 64 doubles per block) to its slot.
-template <int NB, int W>
-__global__ void __launch_bounds__(W * 32) k_hs_gram(HsArgs a, const int* __restrict__ seg_len,
-                                                    const int64_t* __restrict__ seg_beg,
-                                                    const int* __restrict__ seg_slot,
-                                                    double* __restrict__ G) {
-  using C = HsCfg<NB, W>;
-  const int gtid = threadIdx.x, warp = gtid >> 5, lane = gtid & 31;
-  const int seg = blockIdx.x;
-  int pI[C::Q], pJ[C::Q];
-  double acc[C::Q][2];
-  init_pairs<NB, W>(warp, pI, pJ, acc);
-  gram_segment<NB, W>(a, 0, seg_beg[seg], seg_len[seg], gtid, warp, lane, acc, pI, pJ);
-  double* out = G + static_cast<int64_t>(seg_slot[seg]) * C::P * 64;
-#pragma unroll
-  for (int q = 0; q < C::Q; ++q) {
-    const int p = warp + q * W;
-    if (q < C::Q - 1 || p < C::P)
-      *reinterpret_cast<double2*>(out + p * 64 + lane * 2) = make_double2(acc[q][0], acc[q][1]);
+// K1/K2: Gram-only kernel.  The NB(NB+1)/2 lower-triangular 8x8 blocks are
+// split into GR bands of block rows (compile-time, balanced pair counts);
+// warp w owns band w / GK and every GK-th k-step (k-group w % GK).  Per
+// k-step a warp loads each needed 8-row fragment ONCE into registers (the
+// A fragment of block I equals the B fragment of block I) and issues all of
+// its band's DMMAs from registers: ~0.3 shared loads per DMMA instead of 2,
+// which is what lets the FP64 tensor pipe run near its peak.
+template <int NB>
+struct GramShape {
+  static constexpr int P = NB * (NB + 1) / 2;
+  static constexpr int GR = NB <= 9 ? 1 : NB <= 13 ? 2 : NB <= 16 ? 3 : NB <= 19 ? 4 : NB <= 22 ? 6 : 8;
+  static constexpr int GK = GR == 1 ? 4 : GR == 2 ? 2 : 1;
+  static constexpr int W = GR * GK;
+  // first block row of band r (balanced by pair count)
+  static constexpr int band_start(int r) {
+    if (r <= 0) return 0;
+    if (r >= GR) return NB;
+    int acc = 0;
+    for (int I = 0; I < NB; ++I) {
+      if (acc * GR >= r * P) return I;
+      acc += I + 1;
+    }
+    return NB;
   }
+  static constexpr int band_pairs(int r) {
+    const int a = band_start(r), b = band_start(r + 1);
+    return b * (b + 1) / 2 - a * (a + 1) / 2;
+  }
+  static constexpr int max_pairs() {
+    int m = 0;
+    for (int r = 0; r < GR; ++r) m = band_pairs(r) > m ? band_pairs(r) : m;
+    return m;
+  }
+  static constexpr int MAXP = max_pairs();
+};
+
+template <int NB, int R>
+__device__ __forceinline__ void gram_band_kstep(int base, double (&acc)[GramShape<NB>::MAXP][2]) {
+  using G = GramShape<NB>;
+  constexpr int I0 = G::band_start(R), I1 = G::band_start(R + 1);
+  double f[I1 > 0 ? I1 : 1];
+#pragma unroll
+  for (int b = 0; b < I1; ++b) f[b] = g_smem[base + 8 * b];
+  int p = 0;
+#pragma unroll
+  for (int I = I0; I < I1; ++I)
+#pragma unroll
+    for (int J = 0; J <= I; ++J) {
+      dmma884(acc[p][0], acc[p][1], f[I], f[J]);
+      ++p;
+    }
+}
+
+template <int NB, int R>
+__device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len, int kgroup,
+                                          int lane, double (&acc)[GramShape<NB>::MAXP][2]) {
+  using G = GramShape<NB>;
+  using C = HsCfg<NB, G::W>;
+  constexpr int BUF = C::CH * C::LDS;
+  const int gtid = threadIdx.x;
+  const int ld = a.ld;
+  const int nch = ld >> 1;
+  const int padw = C::LDS - ld;
+  for (int e = gtid; e < 2 * C::CH * padw; e += C::GT) {
+    const int t = e / padw, c = e - t * padw;
+    g_smem[t * C::LDS + ld + c] = 0.0;
+  }
+  __syncthreads();
+  auto issue = [&](int s, int bo) {
+    const int base = s * C::CH;
+    const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
+    for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
+      const int c = c0 + gtid;
+      const int t = min(c / nch, C::CH - 1), k = c - t * nch;
+      const int j = __shfl_sync(kFull, jv, t);
+      if (c < C::CH * nch) {
+        double* dst = &g_smem[bo + t * C::LDS + 2 * k];
+        if (base + t < len)
+          cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
+        else
+          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+      }
+    }
+    for (int t = gtid; t < C::CH; t += C::GT) {
+      const int rt = base + t;
+      g_smem[bo + t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
+    }
+  };
+  const int lofs = (lane & 3) * C::LDS + (lane >> 2);
+  const int nst = (len + C::CH - 1) / C::CH;
+  if (nst > 0) issue(0, 0);
+  cp_async_commit();
+  for (int s = 0; s < nst; ++s) {
+    if (s + 1 < nst) {
+      issue(s + 1, ((s + 1) & 1) * BUF);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int bo = (s & 1) * BUF + lofs;
+#pragma unroll
+    for (int kk = kgroup; kk < C::CH / 4; kk += G::GK) gram_band_kstep<NB, R>(bo + kk * 4 * C::LDS, acc);
+    __syncthreads();
+  }
+}
+
+template <int NB, int R>
+__device__ __forceinline__ void gram_band_out(int kgroup, int lane, double* out,
+                                              double (&acc)[GramShape<NB>::MAXP][2]) {
+  using G = GramShape<NB>;
+  constexpr int I0 = G::band_start(R);
+  constexpr int NP = G::band_pairs(R);
+  constexpr int p0 = I0 * (I0 + 1) / 2;
+  // k-groups > 0 park their partials in shared memory; k-group 0 adds them in
+  // k-group order (deterministic) and writes the band's canonical blocks.
+  double* park = g_smem + R * (G::GK - 1) * G::MAXP * 64;
+  if (kgroup > 0) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      *reinterpret_cast<double2*>(park + ((kgroup - 1) * G::MAXP + p) * 64 + lane * 2) =
+          make_double2(acc[p][0], acc[p][1]);
+  }
+  __syncthreads();
+  if (kgroup == 0) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      double2 v = make_double2(acc[p][0], acc[p][1]);
+      for (int g = 1; g < G::GK; ++g) {
+        const double2 u = *reinterpret_cast<const double2*>(park + ((g - 1) * G::MAXP + p) * 64 + lane * 2);
+        v.x += u.x;
+        v.y += u.y;
+      }
+      *reinterpret_cast<double2*>(out + (p0 + p) * 64 + lane * 2) = v;
+    }
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(GramShape<NB>::W * 32)
+    k_hs_gram(HsArgs a, const int* __restrict__ seg_len, const int64_t* __restrict__ seg_beg,
+              const int* __restrict__ seg_slot, double* __restrict__ G) {
+  using GS = GramShape<NB>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int band = warp / GS::GK, kgroup = warp % GS::GK;
+  const int seg = blockIdx.x;
+  const int64_t beg = seg_beg[seg];
+  const int len = seg_len[seg];
+  double* out = G + static_cast<int64_t>(seg_slot[seg]) * GS::P * 64;
+  double acc[GS::MAXP][2];
+#pragma unroll
+  for (int p = 0; p < GS::MAXP; ++p) acc[p][0] = acc[p][1] = 0.0;
+  // one fully specialised body per band (compile-time fragment indices)
+#define AB2_BAND(R)                                              \
+  if (band == R && R < GS::GR) {                                 \
+    gram_band<NB, (R < GS::GR ? R : 0)>(a, beg, len, kgroup, lane, acc); \
+    gram_band_out<NB, (R < GS::GR ? R : 0)>(kgroup, lane, out, acc);     \
+  }
+  AB2_BAND(0) AB2_BAND(1) AB2_BAND(2) AB2_BAND(3) AB2_BAND(4) AB2_BAND(5) AB2_BAND(6) AB2_BAND(7)
+#undef AB2_BAND
 }
 
 struct SolveArgs {
@@ -782,11 +921,14 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     using SC = SolveCfg<NB>;
     const size_t slot_bytes = sizeof(double) * C::P * 64;
     const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
-    const size_t gsmem = sizeof(double) * 2 * C::CH * C::LDS;
+    using GS = GramShape<NB>;
+    using GC = HsCfg<NB, GS::W>;
+    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * GC::CH * GC::LDS,
+                                                           size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
     const size_t ssmem = sizeof(double) * SC::PER_WARP * SC::WPB;
     static bool attr_set = false;
     if (!attr_set) {
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       AB2_CUDA(cudaFuncSetAttribute(k_hs_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr_set = true;
     }
@@ -794,7 +936,7 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     for (const HsBatch& b : P.batches) {
       if (b.seg1 > b.seg0) {
         const int tok = ctx->begin_launch("halfsweep_gram");
-        k_hs_gram<NB, GW><<<b.seg1 - b.seg0, GW * 32, gsmem, ctx->stream>>>(
+        k_hs_gram<NB><<<b.seg1 - b.seg0, GS::W * 32, gsmem, ctx->stream>>>(
             a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
         ctx->end_launch(tok);
       }
