@@ -529,9 +529,73 @@ __device__ __forceinline__ int pidx(int I, int J) { return I * (I + 1) / 2 + J; 
 __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r >> 1) & 1))); }
 
 // K3: batched solve.  One warp per column: sums the column's partial Grams
-// (slot order), adds lambda*n_c, then a right-looking blocked LDL^T on the
-// augmented matrix (8-column panels factored in registers with shuffles,
-// trailing updates on the FP64 tensor cores), then back substitution.
+// (slot order) into a swizzled shared copy, adds lambda*n_c, then a
+// LEFT-looking blocked LDL^T over 8-column block columns J (compile-time
+// recursion, so every block index is static and nothing is predicated):
+// block column J is loaded once into registers, updated by all earlier
+// panels K < J with DMMA (C -= L_K * (D_K^-1 L_K)^T), factored in registers
+// (8 pivots, warp shuffles) and stored once.  The augmented rhs row rides
+// along as the last block row, so forward substitution is free; the back
+// substitution walks the 8-row panels from the bottom.
+template <int NB, int J>
+__device__ __forceinline__ bool ldl_column(double* M, double* dinv, int n_f, int lane) {
+  if constexpr (J >= NB) {
+    return true;
+  } else {
+    if (8 * J >= n_f) return true;
+    constexpr int NI = NB - J;  // block rows J..NB-1
+    const int r = lane >> 2, q = lane & 3;
+    double cv[NI][2];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const double2 v = *reinterpret_cast<const double2*>(M + pidx(J + i, J) * 64 + swz(r, 2 * q));
+      cv[i][0] = v.x;
+      cv[i][1] = v.y;
+    }
+    // updates from every earlier panel (runtime K, static block rows)
+    for (int K = 0; K < J; ++K) {
+      const double* bj = M + (pidx(J, 0) + K) * 64;
+      const double b0 = bj[swz(r, q)] * dinv[8 * K + q];
+      const double b1 = bj[swz(r, 4 + q)] * dinv[8 * K + 4 + q];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const double* ai = M + (pidx(J + i, 0) + K) * 64;
+        dmma884(cv[i][0], cv[i][1], -ai[swz(r, q)], b0);
+        dmma884(cv[i][0], cv[i][1], -ai[swz(r, 4 + q)], b1);
+      }
+    }
+    // factor the panel in registers
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int k = 8 * J + c;
+      if (k >= n_f) {
+        if (lane == 0) dinv[k] = 0.0;  // non-pivot columns contribute nothing
+        continue;
+      }
+      const double d = __shfl_sync(kFull, cv[0][c & 1], 4 * c + (c >> 1));
+      const double cr0 = __shfl_sync(kFull, cv[0][c & 1], 8 * q + (c >> 1));
+      const double cr1 = __shfl_sync(kFull, cv[0][c & 1], 8 * q + 4 + (c >> 1));
+      double aik[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) aik[i] = __shfl_sync(kFull, cv[i][c & 1], 4 * r + (c >> 1));
+      if (!(d > 0.0)) return false;  // Eigen LLT: NumericalIssue on a non-positive pivot
+      const double inv = 1.0 / d;
+      if (lane == 0) dinv[k] = inv;
+      const double cv0 = cr0 * inv, cv1 = cr1 * inv;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        if (2 * q > c) cv[i][0] = fma(-aik[i], cv0, cv[i][0]);
+        if (2 * q + 1 > c) cv[i][1] = fma(-aik[i], cv1, cv[i][1]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      *reinterpret_cast<double2*>(M + pidx(J + i, J) * 64 + swz(r, 2 * q)) = make_double2(cv[i][0], cv[i][1]);
+    __syncwarp();
+    return ldl_column<NB, J + 1>(M, dinv, n_f, lane);
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
     k_hs_solve(HsArgs a, SolveArgs s) {
@@ -564,6 +628,7 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
     const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
     if (ns == 1) {
       // one slot: bulk 16-byte async copies straight into the swizzled blocks
+#pragma unroll 8
       for (int p = 0; p < C::P; ++p) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
       cp_async_commit();
       cp_async_wait<0>();
@@ -580,95 +645,19 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
     }
     __syncwarp();
     // lambda * n_c on the diagonal (als.cpp:58-59): lane (r, q) owns (r, 2q+e)
+#pragma unroll
     for (int I = 0; I < NB; ++I)
       if (8 * I + r < n_f && (r >> 1) == q) M[pidx(I, I) * 64 + swz(r, r)] += shift;
   }
   __syncwarp();
-  const int KP = (n_f + 7) / 8;
-  bool ok = true;
-  for (int K = 0; K < KP && ok; ++K) {
-    double pv[NB][2];
-#pragma unroll
-    for (int i = 0; i < NB; ++i)
-      if (K + i < NB) {
-        const double2 v = *reinterpret_cast<const double2*>(M + pidx(K + i, K) * 64 + swz(r, 2 * q));
-        pv[i][0] = v.x;
-        pv[i][1] = v.y;
-      }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int k = 8 * K + c;
-      if (k >= n_f) break;
-      // all shuffles of the step first (none depends on the pivot), then 1/d
-      const double d = __shfl_sync(kFull, pv[0][c & 1], 4 * c + (c >> 1));
-      const double cr0 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + (c >> 1));
-      const double cr1 = __shfl_sync(kFull, pv[0][c & 1], 8 * q + 4 + (c >> 1));
-      double aik[NB];
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (K + i < NB) aik[i] = __shfl_sync(kFull, pv[i][c & 1], 4 * r + (c >> 1));
-      if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
-        ok = false;
-        break;
-      }
-      const double inv = 1.0 / d;
-      if (lane == 0) dinv[k] = inv;
-      const double cv0 = cr0 * inv, cv1 = cr1 * inv;
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (K + i < NB) {
-          if (2 * q > c) pv[i][0] = fma(-aik[i], cv0, pv[i][0]);
-          if (2 * q + 1 > c) pv[i][1] = fma(-aik[i], cv1, pv[i][1]);
-        }
-    }
-    if (!ok) break;
-#pragma unroll
-    for (int i = 0; i < NB; ++i)
-      if (K + i < NB)
-        *reinterpret_cast<double2*>(M + pidx(K + i, K) * 64 + swz(r, 2 * q)) =
-            make_double2(pv[i][0], pv[i][1]);
-    if (lane < 8 && 8 * K + lane >= n_f) dinv[8 * K + lane] = 0.0;  // non-pivot columns
-    __syncwarp();
-    if (K + 1 < KP) {
-      const double dk0 = dinv[8 * K + q], dk1 = dinv[8 * K + 4 + q];
-      double af[NB][2];
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (K + i < NB) {
-          const double* blk = M + pidx(K + i, K) * 64;
-          af[i][0] = -blk[swz(r, q)];
-          af[i][1] = -blk[swz(r, 4 + q)];
-        }
-      for (int J = K + 1; J < KP; ++J) {
-        const double* bj = M + pidx(J, K) * 64;
-        const double b0 = bj[swz(r, q)] * dk0, b1 = bj[swz(r, 4 + q)] * dk1;
-        // explicit load -> MMA -> store phases so the block updates overlap
-        double2 cv[NB];
-#pragma unroll
-        for (int i = 1; i < NB; ++i)
-          if (K + i >= J && K + i < NB)
-            cv[i] = *reinterpret_cast<const double2*>(M + pidx(K + i, J) * 64 + swz(r, 2 * q));
-#pragma unroll
-        for (int i = 1; i < NB; ++i)
-          if (K + i >= J && K + i < NB) dmma884(cv[i].x, cv[i].y, af[i][0], b0);
-#pragma unroll
-        for (int i = 1; i < NB; ++i)
-          if (K + i >= J && K + i < NB) dmma884(cv[i].x, cv[i].y, af[i][1], b1);
-#pragma unroll
-        for (int i = 1; i < NB; ++i)
-          if (K + i >= J && K + i < NB)
-            *reinterpret_cast<double2*>(M + pidx(K + i, J) * 64 + swz(r, 2 * q)) = cv[i];
-      }
-    }
-    __syncwarp();
-  }
-  if (!ok) {
+  if (!ldl_column<NB, 0>(M, dinv, n_f, lane)) {
     if (lane == 0) {
       a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
       atomicAdd(a.fb_total, 1u);
     }
     return;
   }
+  const int KP = (n_f + 7) / 8;
   // Back substitution: u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k, one
   // 8-row panel at a time: the panel's 8 unknowns by shuffles in lanes 0..7,
   // then every lane folds them into the remaining right-hand side.
