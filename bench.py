@@ -1,0 +1,322 @@
+#!/usr/bin/env python3
+"""bench.py -- ratings/s per ALS-NCG iteration on the B200 core (BASELINE.json).
+
+Workload (N=1): BASELINE config 1 -- 138,493 users x 26,744 items, 20,000,263
+ratings (seeded synthetic stand-in with MovieLens-20M's shape),
+n_f = 100, lambda = 0.01, FP64.  A "step" is one outer ALS-NCG iteration
+(ncg.cpp:194-297): gradient, two half-sweeps (P(x)), quartic line search,
+fused vector work.  value = nnz * K / (device time of K iterations, max over
+ranks).  Inputs (CSR/CSC 480 MB, factor vectors 132 MB each) exceed the
+126 MB L2, so no explicit flush is needed between iterations.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Under torchrun (N>1) every rank owns an nnz-balanced shard of users/items
+and all-gathers factor shards over NCCL; the config is fixed, so scaling is
+"strong".  --impl reference times the reference's own CPU implementation
+(oracle/_ref: the reference sources compiled in place; else the oracle port)
+on a bounded sample of the same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_INDEX = 1
+FP64_PEAK_TFLOPS = 37.1  # DMMA.8x8x4 full-chip, tools/fp64_peak.cu on this pool (profiles/fp64_peak.txt)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.samples, self.stop = device, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------- CPU baseline --
+def cpu_reference_run(steps, sample_users=None):
+    """Reference CPU implementation on a bounded sample of config 1: the
+    first `sample_users` users (all their ratings, all items), n_f = 100,
+    n_workers = n_blocks = nproc, paper_timing (trace loss excluded).
+    Returns (ratings/s per iteration, info dict)."""
+    import numpy as np
+
+    import paper_1508_03110_b200 as P
+    from oracle.pyoracle import Oracle, OracleRatings, make_config, ref_available
+    c = P.CONFIGS[CONFIG_INDEX]
+    cores = os.cpu_count() or 1
+    if sample_users is None:
+        sample_users = max(2000, int(c["n_u"] * min(1.0, 0.02 * cores)))
+    R = P.generate(CONFIG_INDEX, scale_users=sample_users)
+    O = OracleRatings.from_csr(R.n_users(), R.n_items(), R.uptr, R.uidx, R.uval)
+    kind = "ref" if ref_available() else "port"
+    orc = Oracle(kind)
+    iters = max(2, steps + 1)
+    cfg = make_config(lambda_=c["lam"], n_f=c["n_f"], max_iters=iters, tol=0.0, seed=0,
+                      n_workers=cores, n_blocks=cores, paper_timing=1)
+    t0 = time.time()
+    _, trace, _ = orc.ncg_solve(O, cfg)
+    wall = time.time() - t0
+    el = [t["elapsed_seconds"] for t in trace]
+    deltas = [el[k] - el[k - 1] for k in range(2, len(el))] or [el[-1]]
+    per_iter = sum(deltas) / len(deltas)
+    value = R.nnz() / per_iter
+    return value, {"kind": "reference" if kind == "ref" else "port", "cores": cores,
+                   "sample": (f"config 1 users [0,{sample_users}) = {R.nnz()} ratings x 26,744 items, "
+                              f"n_f=100, {iters} ALS-NCG iterations, mean of trace deltas k>=2, "
+                              f"{wall:.1f}s wall"),
+                   "iterations": iters}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    c = __import__("paper_1508_03110_b200").CONFIGS[CONFIG_INDEX]
+    value, info = cpu_reference_run(args.steps)
+    line = {"impl": "reference", "metric": "ratings/s per ALS-NCG iteration", "value": value,
+            "unit": "ratings/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 20_000_263 / value * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, MovieLens-20M shape)",
+            "config": {"workload": "BASELINE config 1 (sampled on CPU)", "n_users": c["n_u"],
+                       "n_items": c["n_m"], "nnz": c["nnz"], "n_f": c["n_f"], "lambda": c["lam"]},
+            "cpu_baseline": {"value": value, "unit": "ratings/s", "cores": info["cores"],
+                             "kind": info["kind"], "sample": info["sample"]},
+            "e2e": {"value": value, "unit": "ratings/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm --
+def gram_flops_per_iteration(R, n_f):
+    # algorithmic Gram+rhs flops of both half-sweeps: 2 * nnz * (f^2 + 3f)
+    return 2.0 * R.nnz() * (n_f * n_f + 3 * n_f)
+
+
+def run_gpu(args):
+    import ctypes as C
+
+    import numpy as np
+
+    import paper_1508_03110_b200 as P
+    from paper_1508_03110_b200 import _lib
+    world, rank, local = dist_env()
+    c = P.CONFIGS[CONFIG_INDEX]
+    n_f, lam = c["n_f"], c["lam"]
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ids = [P.Context.nccl_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(ids, src=0)
+        ctx = P.Context(local, rank, world, ids[0])
+        dist = td
+    else:
+        ctx = P.Context(0)
+
+    t0 = time.time()
+    R = P.generate(CONFIG_INDEX)
+    gen_s = time.time() - t0
+    cfg = P.SolverConfig(lambda_=lam, n_f=n_f, max_iters=1_000_000, tol=0.0, seed=0)
+
+    def barrier():
+        ctx.synchronize()
+        if dist is not None:
+            import torch
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    # ---- device-resident timing (value) ----
+    R.device(ctx)
+    solver = P.ncg.Solver(R, cfg, ctx=ctx)
+    for _ in range(args.warmup):
+        solver.step(1)
+    ctx.synchronize()
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", ctx.device))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    barrier()
+    launches0 = ctx.launches()
+    with ClockSampler(ctx.device) as clk:
+        ev0.record(stream)
+        ran = solver.step(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    launches = ctx.launches() - launches0
+    dev_ms = ev0.elapsed_time(ev1)
+    ctx.set_profiling(False)
+    stats = ctx.kernel_stats()
+    if dist is not None:
+        t = torch.tensor([dev_ms], device=torch.device("cuda", ctx.device))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    assert ran == args.steps, ran
+    per_step_ms = dev_ms / args.steps
+    value = R.nnz() * args.steps / (dev_ms / 1e3)
+    state = solver.state()
+    solver.close()
+
+    # roofline of the dominant kernel (by device time)
+    dom = max(stats.items(), key=lambda kv: kv[1][1]) if stats else ("none", (0, 0.0))
+    gram_ms = stats.get("halfsweep_gram", (0, 0.0))[1]
+    gram_launches = stats.get("halfsweep_gram", (0, 0.0))[0]
+    gram_flops = gram_flops_per_iteration(R, n_f) * args.steps / world
+    achieved = gram_flops / (gram_ms / 1e3) / 1e12 if gram_ms else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gram_dram_bytes_per_launch.txt")
+    if os.path.exists(tp):
+        try:
+            traffic = float(open(tp).read().split()[0])
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "halfsweep_gram (K1/K2: DMMA Gram of both half-sweeps)", "bound": "tensor",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic,
+                "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/fp64_peak.txt); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "algorithmic_flops_per_launch": gram_flops / max(gram_launches, 1),
+                "avg_launch_ms": gram_ms / max(gram_launches, 1),
+                "dominant_by_time": dom[0]}
+    kernels = {k: {"launches": n, "ms_per_step": ms / args.steps} for k, (n, ms) in stats.items()}
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        host = [pin(R.uptr), pin(R.uidx), pin(R.uval), pin(R.iptr), pin(R.iidx), pin(R.ival)]
+        h2d = sum(t.numel() * t.element_size() for t in host)
+        e2e_iters = args.steps
+        model = torch.empty(n_f * (R.n_users() + R.n_items()), dtype=torch.float64).pin_memory()
+        ccfg = P.SolverConfig(lambda_=lam, n_f=n_f, max_iters=e2e_iters, tol=0.0, seed=0,
+                              paper_timing=True).to_c()
+        recs = (_lib.TraceRecordC * (e2e_iters + 2))()
+        res = _lib.ResultC()
+        n = C.c_int(0)
+        L = _lib.lib()
+        t0 = time.perf_counter()
+        h = C.c_void_p()
+        _lib.check(L.alsncg_ratings_upload(ctx.handle, R.n_users(), R.n_items(), R.nnz(),
+                                           *[C.c_void_p(t.data_ptr()) for t in host], C.byref(h)))
+        _lib.check(L.alsncg_ncg_solve(h, C.byref(ccfg), _lib.SNAPSHOT_FN(), None, C.byref(res),
+                                      C.c_void_p(model.data_ptr()), recs, e2e_iters + 2, C.byref(n)))
+        _lib.check(L.alsncg_ratings_free(h))
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": R.nnz() * e2e_iters / e2e_s, "unit": "ratings/s",
+               "h2d_bytes_per_step": h2d / e2e_iters,
+               "d2h_bytes_per_step": model.numel() * 8 / e2e_iters,
+               "note": (f"one alsncg_ratings_upload + alsncg_ncg_solve(max_iters={e2e_iters}) + model "
+                        f"download from pinned host buffers per measurement, incl. setup "
+                        f"(x0, gradient, P(x0)); bytes are per ALS-NCG iteration")}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, info = cpu_reference_run(2)
+        cpu = {"value": v, "unit": "ratings/s", "cores": info["cores"], "kind": info["kind"],
+               "sample": info["sample"]}
+
+    if rank == 0:
+        line = {"metric": "ratings/s per ALS-NCG iteration", "value": value, "unit": "ratings/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": per_step_ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generator, MovieLens-20M shape; dataset not available)",
+                "config": {"workload": "BASELINE config 1: ALS-NCG, 138,493 users x 26,744 items, "
+                                       "20,000,263 ratings, n_f=100, lambda=0.01",
+                           "n_users": R.n_users(), "n_items": R.n_items(), "nnz": R.nnz(),
+                           "n_f": n_f, "lambda": lam, "l2": "inputs > 126 MB L2 (no flush needed)",
+                           "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+                "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+                "clocks": clk.summary(), "kernels": kernels,
+                "solver_state": {k: state[k] for k in ("iterations", "grad_norm", "restarts",
+                                                       "fallback_steps")},
+                "generate_seconds": gen_s}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
