@@ -172,7 +172,7 @@ int alsncg_ctx_create(int device, alsncg_ctx** out) {
 int alsncg_nccl_unique_id(unsigned char id[128]) {
   return guarded([&] {
     ncclUniqueId u;
-    AB2_NCCL(ncclGetUniqueId(&u));
+    AB2_NCCL(ab2::nccl().GetUniqueId(&u));
     static_assert(sizeof(u) == 128, "ncclUniqueId size");
     std::memcpy(id, &u, 128);
   });
@@ -189,7 +189,7 @@ int alsncg_ctx_create_dist(int device, int rank, int world, const unsigned char 
     if (world > 1) {
       ncclUniqueId u;
       std::memcpy(&u, id, 128);
-      AB2_NCCL(ncclCommInitRank(&c->impl->comm, world, u, rank));
+      AB2_NCCL(ab2::nccl().CommInitRank(&c->impl->comm, world, u, rank));
     }
     *out = c.release();
   });

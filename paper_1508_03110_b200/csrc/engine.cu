@@ -38,7 +38,7 @@ Ctx::~Ctx() {
   cudaFree(d_counters);
   cudaFree(d_scalars);
   cudaFreeHost(h_scalars);
-  if (comm) ncclCommDestroy(comm);
+  if (comm) nccl().CommDestroy(comm);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -128,14 +128,14 @@ std::vector<int> partition_rows(int n_rows, const int64_t* ptr, int world, int a
 
 void allgather_rows(Ctx* ctx, double* rows, const std::vector<int>& bounds, int ld) {
   if (ctx->world <= 1) return;
-  AB2_NCCL(ncclGroupStart());
+  AB2_NCCL(nccl().GroupStart());
   for (int r = 0; r < ctx->world; ++r) {
     const size_t count = static_cast<size_t>(bounds[r + 1] - bounds[r]) * ld;
     if (count == 0) continue;
     double* p = rows + static_cast<size_t>(bounds[r]) * ld;
-    AB2_NCCL(ncclBroadcast(p, p, count, ncclDouble, r, ctx->comm, ctx->stream));
+    AB2_NCCL(nccl().Broadcast(p, p, count, ncclDouble, r, ctx->comm, ctx->stream));
   }
-  AB2_NCCL(ncclGroupEnd());
+  AB2_NCCL(nccl().GroupEnd());
 }
 
 // -------------------------------------------------------------- upload --
@@ -358,7 +358,7 @@ std::pair<int64_t, int64_t> DevRatings::routing_totals(int n_blocks) {
   unsigned long long* d = static_cast<unsigned long long*>(ctx->scratch(5, 16));
   launch_routing_count(*this, n_blocks, d);
   if (ctx->world > 1)
-    AB2_NCCL(ncclAllReduce(d, d, 2, ncclUint64, ncclSum, ctx->comm, ctx->stream));
+    AB2_NCCL(nccl().AllReduce(d, d, 2, ncclUint64, ncclSum, ctx->comm, ctx->stream));
   unsigned long long h[2];
   AB2_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "alsncg_capi.h"
+#include "nccl_shim.h"
 
 namespace ab2 {
 
@@ -34,11 +35,12 @@ struct Error : std::runtime_error {
                          std::string(#expr) + ": " + cudaGetErrorString(e_));           \
   } while (0)
 
-#define AB2_NCCL(expr)                                                                     \
-  do {                                                                                     \
-    ncclResult_t r_ = (expr);                                                              \
-    if (r_ != ncclSuccess)                                                                 \
-      throw ::ab2::Error(ALSNCG_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+#define AB2_NCCL(expr)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (expr);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      throw ::ab2::Error(ALSNCG_ENCCL,                                                   \
+                         std::string(#expr) + ": " + ::ab2::nccl().GetErrorString(r_)); \
   } while (0)
 
 inline int row_stride(int n_f) { return (n_f + 1) & ~1; }
