@@ -112,6 +112,37 @@ void Ctx::fetch_scalars(int n) {
   AB2_CUDA(cudaStreamSynchronize(stream));
 }
 
+L2Window::L2Window(Ctx* c, const void* base, size_t bytes) : ctx(c) {
+  static int max_persist = -1, max_window = 0;
+  if (max_persist < 0) {
+    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device) != cudaSuccess)
+      max_persist = 0;
+    if (cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device) != cudaSuccess)
+      max_window = 0;
+    if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
+    cudaGetLastError();
+  }
+  if (max_persist <= 0 || max_window <= 0 || bytes == 0) return;
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  v.accessPolicyWindow.num_bytes = std::min(bytes, static_cast<size_t>(max_window));
+  v.accessPolicyWindow.hitRatio =
+      std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(v.accessPolicyWindow.num_bytes));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  set = cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+  cudaGetLastError();
+}
+
+L2Window::~L2Window() {
+  if (!set) return;
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.num_bytes = 0;
+  cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaCtxResetPersistingL2Cache();
+  cudaGetLastError();
+}
+
 // ------------------------------------------------------------ sharding --
 std::vector<int> partition_rows(int n_rows, const int64_t* ptr, int world, int align) {
   std::vector<int> b(world + 1, 0);

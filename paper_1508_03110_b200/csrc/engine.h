@@ -169,6 +169,16 @@ DevRatings* upload_ratings(Ctx* ctx, int n_u, int n_m, int64_t nnz, const int64_
 // nnz-balanced contiguous ranges aligned to `align` rows (identical on every rank).
 std::vector<int> partition_rows(int n_rows, const int64_t* ptr, int world, int align);
 
+// Scoped L2 access-policy window on ctx->stream: marks [base, base+bytes) as
+// persisting (up to the device's persisting-L2 limit) and restores the
+// stream's default policy on exit.
+struct L2Window {
+  Ctx* ctx;
+  bool set = false;
+  L2Window(Ctx* c, const void* base, size_t bytes);
+  ~L2Window();
+};
+
 // ------------------------------------------------------------- kernels --
 // All launchers enqueue on ctx->stream.  Device flat vectors: (n_u+n_m) rows
 // of ld = row_stride(n_f) doubles, user rows first.

@@ -478,7 +478,7 @@ __device__ __forceinline__ void gram_band_out(int kgroup, int lane, double* out,
         v.x += u.x;
         v.y += u.y;
       }
-      *reinterpret_cast<double2*>(out + (p0 + p) * 64 + lane * 2) = v;
+      __stcs(reinterpret_cast<double2*>(out + (p0 + p) * 64 + lane * 2), v);  // streaming: keep L2 for factor rows
     }
   }
 }
@@ -922,6 +922,10 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       attr_set = true;
     }
     double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
+    // Keep the gathered source factor rows resident in L2 while the Gram
+    // stream (written with evict-first stores) passes through.
+    const int n_src = kind == 0 ? R.n_m : R.n_u;
+    L2Window l2(ctx, a.src, sizeof(double) * static_cast<size_t>(n_src) * a.ld);
     for (const HsBatch& b : P.batches) {
       if (b.seg1 > b.seg0) {
         const int tok = ctx->begin_launch("halfsweep_gram");
