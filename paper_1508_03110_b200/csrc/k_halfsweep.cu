@@ -354,8 +354,10 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
 template <int NB>
 struct GramShape {
   static constexpr int P = NB * (NB + 1) / 2;
-  static constexpr int GR = NB <= 9 ? 1 : NB <= 13 ? 2 : NB <= 16 ? 3 : NB <= 19 ? 4 : NB <= 22 ? 6 : 8;
-  static constexpr int GK = GR == 1 ? 4 : GR == 2 ? 2 : 1;
+  // ~24 block pairs per warp (48 accumulator doubles): enough register reuse
+  // per fragment load, and light enough for 3-4 CTAs per SM.
+  static constexpr int GR = (P + 23) / 24 < 1 ? 1 : ((P + 23) / 24 > 8 ? 8 : (P + 23) / 24);
+  static constexpr int GK = GR >= 4 ? 1 : 4 / GR;
   static constexpr int W = GR * GK;
   // first block row of band r (balanced by pair count)
   static constexpr int band_start(int r) {
@@ -504,6 +506,7 @@ __global__ void __launch_bounds__(GramShape<NB>::W * 32)
     gram_band_out<NB, (R < GS::GR ? R : 0)>(kgroup, lane, out, acc);     \
   }
   AB2_BAND(0) AB2_BAND(1) AB2_BAND(2) AB2_BAND(3) AB2_BAND(4) AB2_BAND(5) AB2_BAND(6) AB2_BAND(7)
+  AB2_BAND(8) AB2_BAND(9) AB2_BAND(10) AB2_BAND(11) AB2_BAND(12) AB2_BAND(13) AB2_BAND(14) AB2_BAND(15)
 #undef AB2_BAND
 }
 
