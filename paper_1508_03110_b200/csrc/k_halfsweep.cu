@@ -356,8 +356,8 @@ struct GramShape {
   static constexpr int P = NB * (NB + 1) / 2;
   // ~24 block pairs per warp (48 accumulator doubles): enough register reuse
   // per fragment load, and light enough for 3-4 CTAs per SM.
-  static constexpr int GR = (P + 23) / 24 < 1 ? 1 : ((P + 23) / 24 > 8 ? 8 : (P + 23) / 24);
-  static constexpr int GK = GR >= 4 ? 1 : 4 / GR;
+  static constexpr int GR = NB <= 9 ? 1 : NB <= 13 ? 2 : NB <= 16 ? 3 : NB <= 19 ? 4 : NB <= 22 ? 6 : 8;
+  static constexpr int GK = GR == 1 ? 4 : GR == 2 ? 2 : 1;
   static constexpr int W = GR * GK;
   // first block row of band r (balanced by pair count)
   static constexpr int band_start(int r) {
@@ -405,48 +405,52 @@ __device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len,
   using G = GramShape<NB>;
   using C = HsCfg<NB, G::W>;
   constexpr int BUF = C::CH * C::LDS;
-  const int gtid = threadIdx.x;
+  const int gtid = threadIdx.x, warp = gtid >> 5;
   const int ld = a.ld;
-  const int nch = ld >> 1;
   const int padw = C::LDS - ld;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + 2 * BUF);  // 2 mbarriers after the buffers
   for (int e = gtid; e < 2 * C::CH * padw; e += C::GT) {
     const int t = e / padw, c = e - t * padw;
     g_smem[t * C::LDS + ld + c] = 0.0;
   }
+  if (gtid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_fence_init();
+  }
   __syncthreads();
-  auto issue = [&](int s, int bo) {
+  // Stage s -> buffer s&1: warp 0 gathers the stage's rows with one TMA bulk
+  // copy per rating (lane t copies source row idx[t], ld*8 bytes) completing
+  // on the buffer's mbarrier; missing tail rows are zero-filled and the
+  // rating values go to column ld with ordinary stores.
+  auto issue = [&](int s) {
     const int base = s * C::CH;
-    const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
-    for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
-      const int c = c0 + gtid;
-      const int t = min(c / nch, C::CH - 1), k = c - t * nch;
-      const int j = __shfl_sync(kFull, jv, t);
-      if (c < C::CH * nch) {
-        double* dst = &g_smem[bo + t * C::LDS + 2 * k];
-        if (base + t < len)
-          cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
-        else
-          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+    const int bo = (s & 1) * BUF;
+    const int nv = min(C::CH, len - base);
+    if (warp == 0) {
+      fence_proxy_async_smem();  // prior generic reads of this buffer happen-before the async writes
+      if (lane == 0) mbar_arrive_expect_tx(bar + (s & 1), static_cast<unsigned>(nv) * ld * 8);
+      __syncwarp();
+      for (int t = lane; t < nv; t += 32) {
+        const int j = a.idx[beg + base + t];
+        tma_load_1d(&g_smem[bo + t * C::LDS], a.src + static_cast<int64_t>(j) * ld,
+                    static_cast<unsigned>(ld) * 8, bar + (s & 1));
       }
     }
-    for (int t = gtid; t < C::CH; t += C::GT) {
-      const int rt = base + t;
-      g_smem[bo + t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
+    for (int e = gtid; e < (C::CH - nv) * ld; e += C::GT) {
+      const int t = nv + e / ld, c = e % ld;
+      g_smem[bo + t * C::LDS + c] = 0.0;
     }
+    for (int t = gtid; t < C::CH; t += C::GT)
+      g_smem[bo + t * C::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
   };
   const int lofs = (lane & 3) * C::LDS + (lane >> 2);
   const int nst = (len + C::CH - 1) / C::CH;
-  if (nst > 0) issue(0, 0);
-  cp_async_commit();
+  if (nst > 0) issue(0);
   for (int s = 0; s < nst; ++s) {
-    if (s + 1 < nst) {
-      issue(s + 1, ((s + 1) & 1) * BUF);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    if (s + 1 < nst) issue(s + 1);
+    mbar_wait(bar + (s & 1), (s >> 1) & 1);
+    __syncthreads();  // zero rows / rating column of stage s visible
     const int bo = (s & 1) * BUF + lofs;
 #pragma unroll
     for (int kk = kgroup; kk < C::CH / 4; kk += G::GK) gram_band_kstep<NB, R>(bo + kk * 4 * C::LDS, acc);
@@ -915,7 +919,7 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
     using GS = GramShape<NB>;
     using GC = HsCfg<NB, GS::W>;
-    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * GC::CH * GC::LDS,
+    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * GC::CH * GC::LDS + 2,
                                                            size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
     const size_t ssmem = sizeof(double) * SC::PER_WARP * SC::WPB;
     static bool attr_set = false;
