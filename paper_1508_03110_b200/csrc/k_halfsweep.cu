@@ -351,13 +351,17 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
 // A fragment of block I equals the B fragment of block I) and issues all of
 // its band's DMMAs from registers: ~0.3 shared loads per DMMA instead of 2,
 // which is what lets the FP64 tensor pipe run near its peak.
+constexpr int kGramStage = 64;  // ratings per TMA stage in the Gram kernel
+
 template <int NB>
 struct GramShape {
   static constexpr int P = NB * (NB + 1) / 2;
   // ~24 block pairs per warp (48 accumulator doubles): enough register reuse
   // per fragment load, and light enough for 3-4 CTAs per SM.
-  static constexpr int GR = NB <= 9 ? 1 : NB <= 13 ? 2 : NB <= 16 ? 3 : NB <= 19 ? 4 : NB <= 22 ? 6 : 8;
-  static constexpr int GK = GR == 1 ? 4 : GR == 2 ? 2 : 1;
+  // <= ~48 block pairs (96 accumulator doubles) per warp; the k-steps of a
+  // stage are split over GK warps per band when there are few bands.
+  static constexpr int GR = (P + 47) / 48 < 2 ? 2 : ((P + 47) / 48 > 8 ? 8 : (P + 47) / 48);
+  static constexpr int GK = GR >= 4 ? 1 : 4 / GR;
   static constexpr int W = GR * GK;
   // first block row of band r (balanced by pair count)
   static constexpr int band_start(int r) {
@@ -404,12 +408,13 @@ __device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len,
                                           int lane, double (&acc)[GramShape<NB>::MAXP][2]) {
   using G = GramShape<NB>;
   using C = HsCfg<NB, G::W>;
-  constexpr int BUF = C::CH * C::LDS;
+  constexpr int CH = kGramStage;
+  constexpr int BUF = CH * C::LDS;
   const int gtid = threadIdx.x, warp = gtid >> 5;
   const int ld = a.ld;
   const int padw = C::LDS - ld;
   uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + 2 * BUF);  // 2 mbarriers after the buffers
-  for (int e = gtid; e < 2 * C::CH * padw; e += C::GT) {
+  for (int e = gtid; e < 2 * CH * padw; e += C::GT) {
     const int t = e / padw, c = e - t * padw;
     g_smem[t * C::LDS + ld + c] = 0.0;
   }
@@ -424,9 +429,9 @@ __device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len,
   // on the buffer's mbarrier; missing tail rows are zero-filled and the
   // rating values go to column ld with ordinary stores.
   auto issue = [&](int s) {
-    const int base = s * C::CH;
+    const int base = s * CH;
     const int bo = (s & 1) * BUF;
-    const int nv = min(C::CH, len - base);
+    const int nv = min(CH, len - base);
     if (warp == 0) {
       fence_proxy_async_smem();  // prior generic reads of this buffer happen-before the async writes
       if (lane == 0) mbar_arrive_expect_tx(bar + (s & 1), static_cast<unsigned>(nv) * ld * 8);
@@ -437,15 +442,15 @@ __device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len,
                     static_cast<unsigned>(ld) * 8, bar + (s & 1));
       }
     }
-    for (int e = gtid; e < (C::CH - nv) * ld; e += C::GT) {
+    for (int e = gtid; e < (CH - nv) * ld; e += C::GT) {
       const int t = nv + e / ld, c = e % ld;
       g_smem[bo + t * C::LDS + c] = 0.0;
     }
-    for (int t = gtid; t < C::CH; t += C::GT)
+    for (int t = gtid; t < CH; t += C::GT)
       g_smem[bo + t * C::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
   };
   const int lofs = (lane & 3) * C::LDS + (lane >> 2);
-  const int nst = (len + C::CH - 1) / C::CH;
+  const int nst = (len + CH - 1) / CH;
   if (nst > 0) issue(0);
   for (int s = 0; s < nst; ++s) {
     if (s + 1 < nst) issue(s + 1);
@@ -453,7 +458,7 @@ __device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len,
     __syncthreads();  // zero rows / rating column of stage s visible
     const int bo = (s & 1) * BUF + lofs;
 #pragma unroll
-    for (int kk = kgroup; kk < C::CH / 4; kk += G::GK) gram_band_kstep<NB, R>(bo + kk * 4 * C::LDS, acc);
+    for (int kk = kgroup; kk < CH / 4; kk += G::GK) gram_band_kstep<NB, R>(bo + kk * 4 * C::LDS, acc);
     __syncthreads();
   }
 }
@@ -919,7 +924,7 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
     using GS = GramShape<NB>;
     using GC = HsCfg<NB, GS::W>;
-    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * GC::CH * GC::LDS + 2,
+    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * kGramStage * GC::LDS + 2,
                                                            size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
     const size_t ssmem = sizeof(double) * SC::PER_WARP * SC::WPB;
     static bool attr_set = false;
