@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
 // A fragment of block I equals the B fragment of block I) and issues all of
 // its band's DMMAs from registers: ~0.3 shared loads per DMMA instead of 2,
 // which is what lets the FP64 tensor pipe run near its peak.
-constexpr int kGramStage = 64;  // ratings per TMA stage in the Gram kernel
+constexpr int kGramStage = 32;  // ratings per TMA stage in the Gram kernel
 
 template <int NB>
 struct GramShape {
