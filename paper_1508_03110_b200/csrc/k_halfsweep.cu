@@ -519,6 +519,147 @@ __global__ void __launch_bounds__(GramShape<NB>::W * 32)
 #undef AB2_BAND
 }
 
+// Warp-specialised persistent Gram kernel (the split path's K1/K2).
+//  * warp GR is the producer: for every stage of every segment this CTA owns
+//    it waits for the ring slot to be released, writes the rating column and
+//    zero tail rows, then gathers the stage's source rows with one TMA bulk
+//    copy per rating (cp.async.bulk ... mbarrier::complete_tx);
+//  * warps 0..GR-1 are consumers: warp r owns the compile-time contiguous
+//    range of canonical block pairs [r*P/GR, (r+1)*P/GR), loads each needed
+//    8-row fragment once per k-step and issues its DMMAs from registers; it
+//    releases the slot with an mbarrier arrive.  No CTA-wide barrier in the
+//    main loop; the producer runs ahead across segment boundaries.
+constexpr int kWsStages = 3;
+constexpr int kWsCH = 32;
+
+template <int NB>
+struct WsShape {
+  static constexpr int P = NB * (NB + 1) / 2;
+  static constexpr int GR = P < 8 ? P : ((P + 23) / 24 > 8 ? ((P + 23) / 24 > 16 ? 16 : (P + 23) / 24) : 8);
+  static constexpr int LDS = NB * 8 + 4;
+  static constexpr int BUF = kWsCH * LDS;
+  static constexpr int p_begin(int r) { return r * P / GR; }
+  static constexpr int row_of(int p) {
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= p) ++i;
+    return i;
+  }
+  static constexpr int col_of(int p) { return p - row_of(p) * (row_of(p) + 1) / 2; }
+  static constexpr bool needs(int r, int b) {
+    for (int p = p_begin(r); p < p_begin(r + 1); ++p)
+      if (row_of(p) == b || col_of(p) == b) return true;
+    return false;
+  }
+  static constexpr int max_pairs() {
+    int m = 0;
+    for (int r = 0; r < GR; ++r) m = p_begin(r + 1) - p_begin(r) > m ? p_begin(r + 1) - p_begin(r) : m;
+    return m;
+  }
+  static constexpr int MAXP = max_pairs();
+  static constexpr size_t smem_bytes() {
+    return sizeof(double) * kWsStages * BUF + 2 * kWsStages * sizeof(uint64_t);
+  }
+};
+
+template <int NB, int R>
+__device__ __forceinline__ void ws_kstep(int base, double (&acc)[WsShape<NB>::MAXP][2]) {
+  using S = WsShape<NB>;
+  constexpr int p0 = S::p_begin(R), p1 = S::p_begin(R + 1);
+  double f[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+    if (S::needs(R, b)) f[b] = g_smem[base + 8 * b];
+#pragma unroll
+  for (int p = p0; p < p1; ++p)
+    dmma884(acc[p - p0][0], acc[p - p0][1], f[S::row_of(p)], f[S::col_of(p)]);
+}
+
+template <int NB, int R>
+__device__ __forceinline__ void ws_consumer(const int* __restrict__ seg_len,
+                                            const int* __restrict__ seg_slot, int n_seg,
+                                            double* __restrict__ G, uint64_t* full,
+                                            uint64_t* empty, int lane) {
+  using S = WsShape<NB>;
+  constexpr int p0 = S::p_begin(R), np = S::p_begin(R + 1) - p0;
+  const int lofs = (lane & 3) * S::LDS + (lane >> 2);
+  int it = 0;
+  for (int seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+    double acc[S::MAXP][2];
+#pragma unroll
+    for (int p = 0; p < S::MAXP; ++p) acc[p][0] = acc[p][1] = 0.0;
+    const int nst = (seg_len[seg] + kWsCH - 1) / kWsCH;
+    for (int s = 0; s < nst; ++s, ++it) {
+      const int buf = it % kWsStages;
+      mbar_wait(full + buf, (it / kWsStages) & 1);
+      const int bo = buf * S::BUF + lofs;
+#pragma unroll
+      for (int kk = 0; kk < kWsCH / 4; ++kk) ws_kstep<NB, R>(bo + kk * 4 * S::LDS, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + buf);
+    }
+    double* out = G + static_cast<int64_t>(seg_slot[seg]) * S::P * 64 + p0 * 64 + lane * 2;
+#pragma unroll
+    for (int p = 0; p < np; ++p)
+      __stcs(reinterpret_cast<double2*>(out + p * 64), make_double2(acc[p][0], acc[p][1]));
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
+    k_hs_gram_ws(HsArgs a, const int* __restrict__ seg_len, const int64_t* __restrict__ seg_beg,
+                 const int* __restrict__ seg_slot, int n_seg, double* __restrict__ G) {
+  using S = WsShape<NB>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = a.ld;
+  uint64_t* full = reinterpret_cast<uint64_t*>(g_smem + kWsStages * S::BUF);
+  uint64_t* empty = full + kWsStages;
+  // pad columns ld+1 .. LDS-1 stay zero for the whole kernel
+  const int padw = S::LDS - ld - 1;
+  for (int e = threadIdx.x; e < kWsStages * kWsCH * padw; e += blockDim.x) {
+    const int t = e / padw, c = e - t * padw;
+    g_smem[t * S::LDS + ld + 1 + c] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, S::GR);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == S::GR) {  // ---------------- producer
+    int it = 0;
+    for (int seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+      const int len = seg_len[seg];
+      const int64_t beg = seg_beg[seg];
+      for (int base = 0; base < len; base += kWsCH, ++it) {
+        const int buf = it % kWsStages, use = it / kWsStages;
+        if (use > 0) mbar_wait(empty + buf, (use - 1) & 1);
+        double* B = g_smem + buf * S::BUF;
+        const int nv = min(kWsCH, len - base);
+        const int t = lane;  // kWsCH == 32: one rating per lane
+        B[t * S::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
+        if (t >= nv)
+          for (int c = 0; c < ld; c += 2) *reinterpret_cast<double2*>(B + t * S::LDS + c) = make_double2(0.0, 0.0);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(full + buf, static_cast<unsigned>(nv) * ld * 8);
+        if (t < nv)
+          tma_load_1d(B + t * S::LDS, a.src + static_cast<int64_t>(a.idx[beg + base + t]) * ld,
+                      static_cast<unsigned>(ld) * 8, full + buf);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------ consumers (compile-time band)
+#define AB2_WS(R)                                                                           \
+  if (warp == R && R < S::GR)                                                               \
+    ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, lane);
+  AB2_WS(0) AB2_WS(1) AB2_WS(2) AB2_WS(3) AB2_WS(4) AB2_WS(5) AB2_WS(6) AB2_WS(7)
+  AB2_WS(8) AB2_WS(9) AB2_WS(10) AB2_WS(11) AB2_WS(12) AB2_WS(13) AB2_WS(14) AB2_WS(15)
+#undef AB2_WS
+}
+
 struct SolveArgs {
   int row0;     // first local row of the batch
   int nrows;    // rows in the batch
@@ -930,6 +1071,7 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     static bool attr_set = false;
     if (!attr_set) {
       AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       AB2_CUDA(cudaFuncSetAttribute(k_hs_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr_set = true;
     }
@@ -940,9 +1082,12 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     L2Window l2(ctx, a.src, sizeof(double) * static_cast<size_t>(n_src) * a.ld);
     for (const HsBatch& b : P.batches) {
       if (b.seg1 > b.seg0) {
+        using WS = WsShape<NB>;
+        const int nseg = b.seg1 - b.seg0;
+        const int grid = std::min(nseg, 2 * ctx->sm_count);  // persistent CTAs
         const int tok = ctx->begin_launch("halfsweep_gram");
-        k_hs_gram<NB><<<b.seg1 - b.seg0, GS::W * 32, gsmem, ctx->stream>>>(
-            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
+        k_hs_gram_ws<NB><<<grid, (WS::GR + 1) * 32, WS::smem_bytes(), ctx->stream>>>(
+            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G);
         ctx->end_launch(tok);
       }
       SolveArgs s;
