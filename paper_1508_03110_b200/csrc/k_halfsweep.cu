@@ -535,7 +535,8 @@ constexpr int kWsCH = 32;
 template <int NB>
 struct WsShape {
   static constexpr int P = NB * (NB + 1) / 2;
-  static constexpr int GR = P < 8 ? P : ((P + 23) / 24 > 8 ? ((P + 23) / 24 > 16 ? 16 : (P + 23) / 24) : 8);
+  // ~12 block pairs per consumer warp, 2..8 consumers
+  static constexpr int GR = P < 2 ? 1 : ((P + 11) / 12 < 2 ? 2 : ((P + 11) / 12 > 8 ? 8 : (P + 11) / 12));
   static constexpr int LDS = NB * 8 + 4;
   static constexpr int BUF = kWsCH * LDS;
   static constexpr int p_begin(int r) { return r * P / GR; }
@@ -656,7 +657,6 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
   if (warp == R && R < S::GR)                                                               \
     ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, lane);
   AB2_WS(0) AB2_WS(1) AB2_WS(2) AB2_WS(3) AB2_WS(4) AB2_WS(5) AB2_WS(6) AB2_WS(7)
-  AB2_WS(8) AB2_WS(9) AB2_WS(10) AB2_WS(11) AB2_WS(12) AB2_WS(13) AB2_WS(14) AB2_WS(15)
 #undef AB2_WS
 }
 
@@ -1081,13 +1081,24 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     const int n_src = kind == 0 ? R.n_m : R.n_u;
     L2Window l2(ctx, a.src, sizeof(double) * static_cast<size_t>(n_src) * a.ld);
     for (const HsBatch& b : P.batches) {
-      if (b.seg1 > b.seg0) {
+      if (b.seg1 > b.seg0 && NB <= 20) {
         using WS = WsShape<NB>;
         const int nseg = b.seg1 - b.seg0;
-        const int grid = std::min(nseg, 2 * ctx->sm_count);  // persistent CTAs
+        static int per_sm = 0;
+        if (per_sm == 0) {
+          AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hs_gram_ws<NB>, (WS::GR + 1) * 32,
+                                                                 WS::smem_bytes()));
+          per_sm = std::max(per_sm, 1);
+        }
+        const int grid = std::min(nseg, per_sm * ctx->sm_count);  // persistent CTAs
         const int tok = ctx->begin_launch("halfsweep_gram");
         k_hs_gram_ws<NB><<<grid, (WS::GR + 1) * 32, WS::smem_bytes(), ctx->stream>>>(
             a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G);
+        ctx->end_launch(tok);
+      } else if (b.seg1 > b.seg0) {
+        const int tok = ctx->begin_launch("halfsweep_gram");
+        k_hs_gram<NB><<<b.seg1 - b.seg0, GS::W * 32, gsmem, ctx->stream>>>(
+            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
         ctx->end_launch(tok);
       }
       SolveArgs s;
