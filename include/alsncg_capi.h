@@ -192,6 +192,13 @@ int alsncg_dev_half_sweep(alsncg_ratings* r, int kind, int n_f, const double* d_
 /* Fused vector ops over n doubles (ncg.cpp:118-136, factors.cpp:80-105). */
 int alsncg_dev_dot(alsncg_ctx* ctx, int64_t n, const double* d_x, const double* d_y,
                    double* out);
+/* Reference summation order (one device thread, index order, no FMA):
+ * bit-identical to the reference's dot (factors.cpp:95-103) and beta_bar
+ * (ncg.cpp:118-132).  Backs the API-level host-vector utilities. */
+int alsncg_dev_dot_seq(alsncg_ctx* ctx, int64_t n, const double* d_x, const double* d_y,
+                       double* out);
+int alsncg_dev_beta_bar_seq(alsncg_ctx* ctx, int64_t n, const double* d_gn, const double* d_gp,
+                            const double* d_bn, const double* d_bp, double* out);
 int alsncg_dev_axpby(alsncg_ctx* ctx, int64_t n, double a, const double* d_x, double b,
                      const double* d_y, double* d_out);
 int alsncg_dev_beta_bar(alsncg_ctx* ctx, int64_t n, const double* d_gn, const double* d_gp,

@@ -79,6 +79,8 @@ SIGNATURES = {
     "alsncg_dev_quartic": (i32, [vp, i32, vp, vp, f64, vp]),
     "alsncg_dev_half_sweep": (i32, [vp, i32, i32, vp, f64, vp, ip]),
     "alsncg_dev_dot": (i32, [vp, i64, vp, vp, dp]),
+    "alsncg_dev_dot_seq": (i32, [vp, i64, vp, vp, dp]),
+    "alsncg_dev_beta_bar_seq": (i32, [vp, i64, vp, vp, vp, vp, dp]),
     "alsncg_dev_axpby": (i32, [vp, i64, f64, vp, f64, vp, vp]),
     "alsncg_dev_beta_bar": (i32, [vp, i64, vp, vp, vp, vp, dp]),
     "alsncg_dev_malloc": (i32, [vp, C.c_size_t, C.POINTER(vp)]),

@@ -466,6 +466,30 @@ int alsncg_dev_dot(alsncg_ctx* ctx, int64_t n, const double* d_x, const double* 
   });
 }
 
+int alsncg_dev_dot_seq(alsncg_ctx* ctx, int64_t n, const double* d_x, const double* d_y, double* out) {
+  return guarded([&] {
+    ab2::launch_seq_dots(ctx->impl.get(), n, d_x, d_y, nullptr, nullptr, 0);
+    ctx->impl->fetch_scalars(1);
+    *out = ctx->impl->h_scalars[0];
+  });
+}
+
+int alsncg_dev_beta_bar_seq(alsncg_ctx* ctx, int64_t n, const double* d_gn, const double* d_gp,
+                            const double* d_bn, const double* d_bp, double* out) {
+  return guarded([&] {
+    // num = sum bn*(gn - gp), den = sum bp*gp, each in index order (ncg.cpp:123-131)
+    ab2::launch_seq_dots(ctx->impl.get(), n, d_bn, d_gn, d_gp, d_bp, 0);
+    ctx->impl->fetch_scalars(2);
+    const double num = ctx->impl->h_scalars[0], den = ctx->impl->h_scalars[1];
+    double beta = 0.0;
+    if (!(std::abs(den) < 1e-30)) {
+      beta = num / den;
+      if (!std::isfinite(beta)) beta = 0.0;
+    }
+    *out = beta;
+  });
+}
+
 int alsncg_dev_axpby(alsncg_ctx* ctx, int64_t n, double a, const double* d_x, double b,
                      const double* d_y, double* d_out) {
   return guarded([&] { ab2::launch_axpby(ctx->impl.get(), n, a, d_x, b, d_y, d_out); });

@@ -235,7 +235,7 @@ double dot(const FlatVector& x, const FlatVector& y) {
   const size_t bytes = hx.size() * sizeof(double);
   DevBuf dx(hx.data(), bytes), dy(hy.data(), bytes);
   double out = 0.0;
-  check(alsncg_dev_dot(default_ctx(), static_cast<std::int64_t>(hx.size()), dx.d(), dy.d(), &out));
+  check(alsncg_dev_dot_seq(default_ctx(), static_cast<std::int64_t>(hx.size()), dx.d(), dy.d(), &out));
   return out;
 }
 
@@ -505,7 +505,7 @@ double beta_bar(const FlatVector& g_next, const FlatVector& g_prev, const FlatVe
   const size_t bytes = a.size() * sizeof(double);
   DevBuf da(a.data(), bytes), db(b.data(), bytes), dc(c.data(), bytes), dd(d.data(), bytes);
   double out = 0.0;
-  check(alsncg_dev_beta_bar(default_ctx(), static_cast<std::int64_t>(a.size()), da.d(), db.d(), dc.d(), dd.d(), &out));
+  check(alsncg_dev_beta_bar_seq(default_ctx(), static_cast<std::int64_t>(a.size()), da.d(), db.d(), dc.d(), dd.d(), &out));
   return out;
 }
 

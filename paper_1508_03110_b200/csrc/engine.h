@@ -208,6 +208,10 @@ enum VecOp {
 };
 void launch_vec(Ctx* ctx, VecOp op, int64_t n, const double* a, const double* b,
                 const double* c, const double* d, double beta, double* out, int slot);
+// Reference-order sums (single thread): s0 = sum a*(b - c) (c may be null:
+// sum a*b), s1 = sum d*c (d may be null) into d_scalars[slot], [slot+1].
+void launch_seq_dots(Ctx* ctx, int64_t n, const double* a, const double* b, const double* c,
+                     const double* d, int slot);
 // out = a*x + b*y elementwise (no FMA: reference rounding, factors.cpp:88-91).
 void launch_axpby(Ctx* ctx, int64_t n, double a, const double* x, double b, const double* y,
                   double* out);

@@ -146,6 +146,22 @@ __global__ void k_routing_count(int nrows, const int64_t* __restrict__ ptr,
   if (lane == 0) atomicAdd(out, total);
 }
 
+// Reference summation order (factors.cpp:95-103, ncg.cpp:118-132): one
+// thread walks the vector in index order with separately rounded multiply
+// and add, reproducing the reference's dot / beta_bar bit for bit.  Used by
+// the API-level host-vector utilities only; the driver uses k_vec.
+__global__ void k_seq_dots(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           const double* __restrict__ c, const double* __restrict__ d, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    s0 = __dadd_rn(s0, __dmul_rn(a[i], c ? __dsub_rn(b[i], c[i]) : b[i]));
+    if (d) s1 = __dadd_rn(s1, __dmul_rn(d[i], c[i]));
+  }
+  out[0] = s0;
+  out[1] = s1;
+}
+
 int vec_blocks(int64_t n) {
   int64_t b = (n + kVecThreads * 8 - 1) / (kVecThreads * 8);
   if (b < 1) b = 1;
@@ -194,6 +210,13 @@ void launch_vec(Ctx* ctx, VecOp op, int64_t n, const double* a, const double* b,
       break;
     }
   }
+}
+
+void launch_seq_dots(Ctx* ctx, int64_t n, const double* a, const double* b, const double* c,
+                     const double* d, int slot) {
+  const int t = ctx->begin_launch("vec_seq_dot");
+  k_seq_dots<<<1, 32, 0, ctx->stream>>>(n, a, b, c, d, ctx->d_scalars + slot);
+  ctx->end_launch(t);
 }
 
 void launch_axpby(Ctx* ctx, int64_t n, double a, const double* x, double b, const double* y,

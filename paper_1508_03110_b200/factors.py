@@ -1,7 +1,7 @@
 """FactorModel / FlatVector and the vector operations (factors.hpp:24-91).
 
 axpby/dot/norm run on the device kernels (k_vec.cu): axpby is bitwise the
-reference's a*x + b*y; dot/norm use the deterministic compensated reduction.
+reference's a*x + b*y; dot/norm follow the reference's index order bit for bit.
 """
 from __future__ import annotations
 
@@ -119,7 +119,8 @@ def axpby(a, x, b, y, ctx=None):
 
 
 def dot(x, y, ctx=None):
-    """Euclidean inner product (factors.cpp:95-103), compensated on the device."""
+    """Euclidean inner product in the reference's index order (factors.cpp:95-103,
+    bit-identical; the fused driver uses the compensated k_vec reductions)."""
     import ctypes as C
     from .device import default_context
     if not x.same_shape(y):
@@ -127,7 +128,7 @@ def dot(x, y, ctx=None):
     ctx = ctx or default_context()
     dx, dy = _dev_pair(x, y, ctx)
     out = C.c_double()
-    check(lib().alsncg_dev_dot(ctx.handle, x.size(), dx.ptr, dy.ptr, C.byref(out)))
+    check(lib().alsncg_dev_dot_seq(ctx.handle, x.size(), dx.ptr, dy.ptr, C.byref(out)))
     return out.value
 
 

@@ -53,7 +53,7 @@ def beta_bar(g_next, g_prev, gbar_next, gbar_prev, ctx=None):
     ctx = ctx or default_context()
     bufs = [DeviceBuffer.from_array(ctx, v.array()) for v in (g_next, g_prev, gbar_next, gbar_prev)]
     out = C.c_double()
-    check(lib().alsncg_dev_beta_bar(ctx.handle, g_next.size(), bufs[0].ptr, bufs[1].ptr,
+    check(lib().alsncg_dev_beta_bar_seq(ctx.handle, g_next.size(), bufs[0].ptr, bufs[1].ptr,
                                     bufs[2].ptr, bufs[3].ptr, C.byref(out)))
     return out.value
 

@@ -205,18 +205,26 @@ def test_half_sweep_unregularised_stationarity():
 
 def test_vector_ops_within_8_ulps():
     # test_core.cpp:97-112, test_ncg.cpp:126-154
+    from oracle.pyoracle import beta_bar as orc_beta_bar, dot as orc_dot
+    ctx = P.default_context()
     for seed in range(3):
         x = P.FlatVector.from_array(random_flat(4, 800, 1200, 100 + seed), 4, 800, 1200)
         y = P.FlatVector.from_array(random_flat(4, 800, 1200, 200 + seed), 4, 800, 1200)
+        # API-level dot: the reference's sequential order, bit for bit
+        assert P.dot(x, y) == orc_dot(x.array(), y.array())
+        # driver reduction (compensated): within 8 ulps of the exact sum
+        dx, dy = P.DeviceBuffer.from_array(ctx, x.array()), P.DeviceBuffer.from_array(ctx, y.array())
+        import ctypes as C
+        out = C.c_double()
+        P._lib.check(P.lib().alsncg_dev_dot(ctx.handle, x.size(), dx.ptr, dy.ptr, C.byref(out)))
         exact = float(np.sum(np.longdouble(x.array()) * np.longdouble(y.array())))
-        assert ulps_between(P.dot(x, y), exact) <= 8
+        assert ulps_between(out.value, exact) <= 8
         z = P.axpby(1.5, x, -2.5, y).array()
         assert np.array_equal(z, 1.5 * x.array() + (-2.5) * y.array())  # bitwise
         gn, gp, bn, bp = (P.FlatVector.from_array(random_flat(2, 10, 6, s), 2, 10, 6)
                           for s in (60 + seed, 70 + seed, 80 + seed, 90 + seed))
-        num = float(np.sum(np.longdouble(bn.array()) * (np.longdouble(gn.array()) - gp.array())))
-        den = float(np.sum(np.longdouble(bp.array()) * np.longdouble(gp.array())))
-        assert ulps_between(P.ncg.beta_bar(gn, gp, bn, bp), num / den) <= 8
+        assert P.ncg.beta_bar(gn, gp, bn, bp) == orc_beta_bar(gn.array(), gp.array(), bn.array(),
+                                                              bp.array())
     a = P.FlatVector(1, 2, 0, [1.0, 0.0], [])
     b = P.FlatVector(1, 2, 0, [0.0, 1.0], [])
     assert P.ncg.beta_bar(a, b, a, a) == 0.0  # degenerate denominator restarts
