@@ -683,70 +683,101 @@ __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r 
 
 // K3: batched solve.  One warp per column: sums the column's partial Grams
 // (slot order) into a swizzled shared copy, adds lambda*n_c, then a
-// LEFT-looking blocked LDL^T over 8-column block columns J (compile-time
-// recursion, so every block index is static and nothing is predicated):
-// block column J is loaded once into registers, updated by all earlier
-// panels K < J with DMMA (C -= L_K * (D_K^-1 L_K)^T), factored in registers
-// (8 pivots, warp shuffles) and stored once.  The augmented rhs row rides
-// along as the last block row, so forward substitution is free; the back
-// substitution walks the 8-row panels from the bottom.
-template <int NB, int J>
-__device__ __forceinline__ bool ldl_column(double* M, double* dinv, int n_f, int lane) {
-  if constexpr (J >= NB) {
-    return true;
-  } else {
-    if (8 * J >= n_f) return true;
-    constexpr int NI = NB - J;  // block rows J..NB-1
-    const int r = lane >> 2, q = lane & 3;
-    double cv[NI][2];
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const double2 v = *reinterpret_cast<const double2*>(M + pidx(J + i, J) * 64 + swz(r, 2 * q));
-      cv[i][0] = v.x;
-      cv[i][1] = v.y;
-    }
-    // updates from every earlier panel (runtime K, static block rows)
-    for (int K = 0; K < J; ++K) {
-      const double* bj = M + (pidx(J, 0) + K) * 64;
-      const double b0 = bj[swz(r, q)] * dinv[8 * K + q];
-      const double b1 = bj[swz(r, 4 + q)] * dinv[8 * K + 4 + q];
-#pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        const double* ai = M + (pidx(J + i, 0) + K) * 64;
-        dmma884(cv[i][0], cv[i][1], -ai[swz(r, q)], b0);
-        dmma884(cv[i][0], cv[i][1], -ai[swz(r, 4 + q)], b1);
+// left-looking blocked LDL^T over 8-column block columns J:
+//   (1) C(I,J) -= sum_{K<J} L(I,K) * (D_K^-1 L(J,K))^T on the FP64 tensor
+//       cores, two block rows at a time (independent DMMA chains);
+//   (2) the 8x8 diagonal block is factored by lanes 0..7 (one row each);
+//   (3) the rows below are eliminated lane-parallel (TRSM form, 28 FMAs per
+//       row against the factored diagonal block).
+// Storage is unscaled (A(i,k) = L~(i,k) d_k) so the augmented rhs row is
+// eliminated with the matrix and forward substitution comes for free.
+template <int NB>
+__device__ __forceinline__ bool ldl_factor(double* M, double* dinv, int n_f, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  const int KP = (n_f + 7) / 8;
+  for (int J = 0; J < KP; ++J) {
+    // (1) updates from earlier panels
+    if (J > 0) {
+      for (int I = J; I < NB; I += 2) {
+        const bool two = I + 1 < NB;
+        double* c0p = M + pidx(I, J) * 64 + swz(r, 2 * q);
+        double* c1p = M + pidx(two ? I + 1 : I, J) * 64 + swz(r, 2 * q);
+        double2 c0 = *reinterpret_cast<const double2*>(c0p);
+        double2 c1 = two ? *reinterpret_cast<const double2*>(c1p) : make_double2(0.0, 0.0);
+        const double* bj = M + pidx(J, 0) * 64;
+        const double* a0 = M + pidx(I, 0) * 64;
+        const double* a1 = M + pidx(two ? I + 1 : I, 0) * 64;
+        for (int K = 0; K < J; ++K) {
+          const int o = K * 64;
+          const double b0 = bj[o + swz(r, q)] * dinv[8 * K + q];
+          const double b1 = bj[o + swz(r, 4 + q)] * dinv[8 * K + 4 + q];
+          dmma884(c0.x, c0.y, -a0[o + swz(r, q)], b0);
+          dmma884(c1.x, c1.y, -a1[o + swz(r, q)], b0);
+          dmma884(c0.x, c0.y, -a0[o + swz(r, 4 + q)], b1);
+          dmma884(c1.x, c1.y, -a1[o + swz(r, 4 + q)], b1);
+        }
+        *reinterpret_cast<double2*>(c0p) = c0;
+        if (two) *reinterpret_cast<double2*>(c1p) = c1;
       }
+      __syncwarp();
     }
-    // factor the panel in registers
+    // (2) diagonal block: lane rr < 8 holds row rr of block (J,J)
+    double* D = M + pidx(J, J) * 64;
+    const int rr = lane & 7;
+    double row[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int k = 8 * J + c;
-      if (k >= n_f) {
-        if (lane == 0) dinv[k] = 0.0;  // non-pivot columns contribute nothing
+      if (k >= n_f) {  // non-pivot columns (padding / rhs column)
+        if (lane == 0) dinv[k] = 0.0;
         continue;
       }
-      const double d = __shfl_sync(kFull, cv[0][c & 1], 4 * c + (c >> 1));
-      const double cr0 = __shfl_sync(kFull, cv[0][c & 1], 8 * q + (c >> 1));
-      const double cr1 = __shfl_sync(kFull, cv[0][c & 1], 8 * q + 4 + (c >> 1));
-      double aik[NI];
-#pragma unroll
-      for (int i = 0; i < NI; ++i) aik[i] = __shfl_sync(kFull, cv[i][c & 1], 4 * r + (c >> 1));
+      const double d = __shfl_sync(kFull, row[c], c);
       if (!(d > 0.0)) return false;  // Eigen LLT: NumericalIssue on a non-positive pivot
       const double inv = 1.0 / d;
       if (lane == 0) dinv[k] = inv;
-      const double cv0 = cr0 * inv, cv1 = cr1 * inv;
+      const double l = row[c] * inv;
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        if (2 * q > c) cv[i][0] = fma(-aik[i], cv0, cv[i][0]);
-        if (2 * q + 1 > c) cv[i][1] = fma(-aik[i], cv1, cv[i][1]);
+      for (int c2 = c + 1; c2 < 8; ++c2) {
+        const double a = __shfl_sync(kFull, row[c], c2);  // A(c2, c)
+        if (rr > c && c2 <= rr) row[c2] = fma(-l, a, row[c2]);
       }
     }
+    if (lane < 8)
 #pragma unroll
-    for (int i = 0; i < NI; ++i)
-      *reinterpret_cast<double2*>(M + pidx(J + i, J) * 64 + swz(r, 2 * q)) = make_double2(cv[i][0], cv[i][1]);
+      for (int c = 0; c < 8; ++c)
+        if (c <= rr) D[swz(rr, c)] = row[c];
     __syncwarp();
-    return ldl_column<NB, J + 1>(M, dinv, n_f, lane);
+    // (3) rows below the diagonal block: x_c' -= x_c * A(c',c)/d_c
+    if (J + 1 < NB) {
+      double s[28];
+      {
+        int t = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) s[t++] = D[swz(c2, c)] * dinv[8 * J + c];
+      }
+      for (int i = 8 * (J + 1) + lane; i < 8 * NB; i += 32) {
+        double* rowp = M + pidx(i >> 3, J) * 64;
+        const int ri = i & 7;
+        double x[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = rowp[swz(ri, c)];
+        int t = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], s[t++], x[c2]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) rowp[swz(ri, c)] = x[c];
+      }
+      __syncwarp();
+    }
   }
+  return true;
 }
 
 template <int NB>
@@ -803,7 +834,7 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
       if (8 * I + r < n_f && (r >> 1) == q) M[pidx(I, I) * 64 + swz(r, r)] += shift;
   }
   __syncwarp();
-  if (!ldl_column<NB, 0>(M, dinv, n_f, lane)) {
+  if (!ldl_factor<NB>(M, dinv, n_f, lane)) {
     if (lane == 0) {
       a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
       atomicAdd(a.fb_total, 1u);
