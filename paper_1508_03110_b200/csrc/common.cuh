@@ -128,6 +128,18 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
       : "memory");
 }
 
+// 1/d for a positive normal d: hardware reciprocal seed (MUFU.RCP64H) and two
+// Newton steps -- a short dependency chain instead of the IEEE division
+// subroutine; error <= 1 ulp, used only on Cholesky pivots.
+__device__ __forceinline__ double fast_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+
 // FP64 tensor-core MMA (lowers to SASS DMMA.8x8x4 on sm_100a):
 // D(8x8) += A(8x4) * B(4x8); lane l holds A[l>>2][l&3], B[l&3][l>>2],
 // D[l>>2][2*(l&3) + {0,1}].

@@ -696,28 +696,31 @@ __device__ __forceinline__ bool ldl_factor(double* M, double* dinv, int n_f, int
   const int r = lane >> 2, q = lane & 3;
   const int KP = (n_f + 7) / 8;
   for (int J = 0; J < KP; ++J) {
-    // (1) updates from earlier panels
+    // (1) updates from earlier panels, four block rows per pass (four
+    // independent DMMA accumulation chains)
     if (J > 0) {
-      for (int I = J; I < NB; I += 2) {
-        const bool two = I + 1 < NB;
-        double* c0p = M + pidx(I, J) * 64 + swz(r, 2 * q);
-        double* c1p = M + pidx(two ? I + 1 : I, J) * 64 + swz(r, 2 * q);
-        double2 c0 = *reinterpret_cast<const double2*>(c0p);
-        double2 c1 = two ? *reinterpret_cast<const double2*>(c1p) : make_double2(0.0, 0.0);
-        const double* bj = M + pidx(J, 0) * 64;
-        const double* a0 = M + pidx(I, 0) * 64;
-        const double* a1 = M + pidx(two ? I + 1 : I, 0) * 64;
+      const double* bj = M + pidx(J, 0) * 64;
+      for (int I = J; I < NB; I += 4) {
+        double2 c[4];
+        const double* ap[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int Iu = min(I + u, NB - 1);
+          c[u] = *reinterpret_cast<const double2*>(M + pidx(Iu, J) * 64 + swz(r, 2 * q));
+          ap[u] = M + pidx(Iu, 0) * 64;
+        }
         for (int K = 0; K < J; ++K) {
           const int o = K * 64;
           const double b0 = bj[o + swz(r, q)] * dinv[8 * K + q];
           const double b1 = bj[o + swz(r, 4 + q)] * dinv[8 * K + 4 + q];
-          dmma884(c0.x, c0.y, -a0[o + swz(r, q)], b0);
-          dmma884(c1.x, c1.y, -a1[o + swz(r, q)], b0);
-          dmma884(c0.x, c0.y, -a0[o + swz(r, 4 + q)], b1);
-          dmma884(c1.x, c1.y, -a1[o + swz(r, 4 + q)], b1);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma884(c[u].x, c[u].y, -ap[u][o + swz(r, q)], b0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma884(c[u].x, c[u].y, -ap[u][o + swz(r, 4 + q)], b1);
         }
-        *reinterpret_cast<double2*>(c0p) = c0;
-        if (two) *reinterpret_cast<double2*>(c1p) = c1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (I + u < NB) *reinterpret_cast<double2*>(M + pidx(I + u, J) * 64 + swz(r, 2 * q)) = c[u];
       }
       __syncwarp();
     }
@@ -736,7 +739,7 @@ __device__ __forceinline__ bool ldl_factor(double* M, double* dinv, int n_f, int
       }
       const double d = __shfl_sync(kFull, row[c], c);
       if (!(d > 0.0)) return false;  // Eigen LLT: NumericalIssue on a non-positive pivot
-      const double inv = 1.0 / d;
+      const double inv = fast_rcp(d);
       if (lane == 0) dinv[k] = inv;
       const double l = row[c] * inv;
 #pragma unroll
