@@ -878,6 +878,194 @@ __global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
   for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
 }
 
+// K3 (CTA form): one 4-warp CTA per column, right-looking blocked LDL^T.
+// Per 8-column panel J: (a) lanes 0..7 of warp 0 factor the diagonal block,
+// (b) all threads eliminate the panel rows below it (TRSM form), (c) the
+// four warps apply the panel to the trailing blocks with DMMA
+// (C(I,K) -= L(I,J) (D_J^-1 L(K,J))^T).  Back substitution by warp 0.
+constexpr int kSolveCtaWarps = 4;
+
+template <int NB>
+__global__ void __launch_bounds__(kSolveCtaWarps * 32) k_hs_solve_cta(HsArgs a, SolveArgs s) {
+  using C = SolveCfg<NB>;
+  constexpr int NT = kSolveCtaWarps * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lr = s.row0 + blockIdx.x;
+  const int n_f = a.n_f, ld = a.ld;
+  double* M = g_smem;
+  double* dinv = M + C::P * 64;
+  double* w = dinv + NB * 8;
+  __shared__ int fail;
+  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
+  if (count == 0) {
+    for (int k = tid; k < ld; k += NT) out[k] = 0.0;
+    return;
+  }
+  const double shift = a.lambda * static_cast<double>(count);
+  if (!(shift > 0.0)) {
+    if (tid == 0) {
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  const int r = lane >> 2, q = lane & 3;
+  {
+    const int ns = s.row_nslot[lr];
+    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
+    if (ns == 1) {
+      for (int p = warp; p < C::P; p += kSolveCtaWarps) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
+      cp_async_commit();
+      cp_async_wait<0>();
+    } else {
+      for (int p = warp; p < C::P; p += kSolveCtaWarps) {
+        double2 v = *reinterpret_cast<const double2*>(base + p * 64);
+        for (int t = 1; t < ns; ++t) {
+          const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
+          v.x += u.x;
+          v.y += u.y;
+        }
+        *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
+      }
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int k = tid; k < n_f; k += NT) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;
+    __syncthreads();
+  }
+  const int KP = (n_f + 7) / 8;
+  for (int J = 0; J < KP; ++J) {
+    double* D = M + pidx(J, J) * 64;
+    // (a) diagonal block
+    if (warp == 0) {
+      const int rr = lane & 7;
+      double row[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
+      bool ok = true;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int k = 8 * J + c;
+        if (k >= n_f) {
+          if (lane == 0) dinv[k] = 0.0;
+          continue;
+        }
+        const double d = __shfl_sync(kFull, row[c], c);
+        if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
+          ok = false;
+          break;
+        }
+        const double inv = fast_rcp(d);
+        if (lane == 0) dinv[k] = inv;
+        const double l = row[c] * inv;
+#pragma unroll
+        for (int c2 = c + 1; c2 < 8; ++c2) {
+          const double av = __shfl_sync(kFull, row[c], c2);
+          if (rr > c && c2 <= rr) row[c2] = fma(-l, av, row[c2]);
+        }
+      }
+      if (!ok) {
+        if (lane == 0) fail = 1;
+      } else if (lane < 8) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c <= rr) D[swz(rr, c)] = row[c];
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    // (b) rows below the diagonal block
+    if (J + 1 < NB) {
+      double sc[28];
+      {
+        int t = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) sc[t++] = D[swz(c2, c)] * dinv[8 * J + c];
+      }
+      for (int i = 8 * (J + 1) + tid; i < 8 * NB; i += NT) {
+        double* rowp = M + pidx(i >> 3, J) * 64;
+        const int ri = i & 7;
+        double x[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = rowp[swz(ri, c)];
+        int t = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], sc[t++], x[c2]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) rowp[swz(ri, c)] = x[c];
+      }
+    }
+    __syncthreads();
+    // (c) trailing update by panel J: block columns Kc in (J, KP), rows I in [Kc, NB)
+    if (J + 1 < KP) {
+      const double dk0 = dinv[8 * J + q], dk1 = dinv[8 * J + 4 + q];
+      for (int Kc = J + 1; Kc < KP; ++Kc) {
+        const double* bk = M + pidx(Kc, J) * 64;
+        const double b0 = bk[swz(r, q)] * dk0, b1 = bk[swz(r, 4 + q)] * dk1;
+        for (int I = Kc + warp; I < NB; I += 2 * kSolveCtaWarps) {
+          const int I2 = I + kSolveCtaWarps;
+          const bool two = I2 < NB;
+          const double* a0 = M + pidx(I, J) * 64;
+          const double* a1 = M + pidx(two ? I2 : I, J) * 64;
+          double* c0p = M + pidx(I, Kc) * 64 + swz(r, 2 * q);
+          double* c1p = M + pidx(two ? I2 : I, Kc) * 64 + swz(r, 2 * q);
+          double2 c0 = *reinterpret_cast<const double2*>(c0p);
+          double2 c1 = *reinterpret_cast<const double2*>(c1p);
+          dmma884(c0.x, c0.y, -a0[swz(r, q)], b0);
+          dmma884(c1.x, c1.y, -a1[swz(r, q)], b0);
+          dmma884(c0.x, c0.y, -a0[swz(r, 4 + q)], b1);
+          dmma884(c1.x, c1.y, -a1[swz(r, 4 + q)], b1);
+          *reinterpret_cast<double2*>(c0p) = c0;
+          if (two) *reinterpret_cast<double2*>(c1p) = c1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) {
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  if (warp != 0) return;
+  // Back substitution (warp 0): u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
+  const int IR = ld >> 3, rr = ld & 7;
+  for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
+  __syncwarp();
+  for (int K = KP - 1; K >= 0; --K) {
+    const int kc = 8 * K + (lane & 7);
+    double wk = (lane < 8 && kc < n_f) ? w[kc] : 0.0;
+    const double dk = (lane < 8 && kc < n_f) ? dinv[kc] : 0.0;
+#pragma unroll
+    for (int c = 7; c >= 0; --c) {
+      const double u = __shfl_sync(kFull, wk * dk, c);
+      if (lane < c) wk = fma(-M[pidx(K, K) * 64 + swz(c, lane)], u, wk);
+      if (lane == c) wk = u;
+    }
+    if (lane < 8 && kc < n_f) w[kc] = wk;
+    double uu[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) uu[c] = __shfl_sync(kFull, wk, c);
+    for (int i = lane; i < 8 * K; i += 32) {
+      const double* blk = M + pidx(K, i >> 3) * 64;
+      double acc = w[i];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (8 * K + c < n_f) acc = fma(-blk[swz(c, i & 7)], uu[c], acc);
+      w[i] = acc;
+    }
+    __syncwarp();
+  }
+  for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
+}
+
 // ------------------------------------------------------------ fallback --
 // Least-norm solve for listed rows.  Workspace per CTA: W (n x n), Q (n x n).
 constexpr int kFbThreads = 256;
@@ -1055,6 +1243,7 @@ struct Mode {
 };
 
 constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
+constexpr bool kSolveCta = true;                  // CTA-per-column solve for n_f >= 63
 
 template <int NB>
 void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
@@ -1107,6 +1296,7 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       AB2_CUDA(cudaFuncSetAttribute(k_hs_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_cta<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr_set = true;
     }
     double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
@@ -1142,7 +1332,12 @@ void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       s.row_nslot = P.row_nslot;
       s.G = G;
       const int tok = ctx->begin_launch("halfsweep_solve");
-      k_hs_solve<NB><<<(s.nrows + SC::WPB - 1) / SC::WPB, SC::WPB * 32, ssmem, ctx->stream>>>(a, s);
+      if (kSolveCta && NB >= 9) {
+        const size_t csmem = sizeof(double) * SC::PER_WARP;
+        k_hs_solve_cta<NB><<<s.nrows, kSolveCtaWarps * 32, csmem, ctx->stream>>>(a, s);
+      } else {
+        k_hs_solve<NB><<<(s.nrows + SC::WPB - 1) / SC::WPB, SC::WPB * 32, ssmem, ctx->stream>>>(a, s);
+      }
       ctx->end_launch(tok);
     }
   }
