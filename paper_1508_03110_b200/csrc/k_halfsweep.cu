@@ -1,1070 +1,13 @@
-// k_halfsweep.cu -- K1-K4: one ALS half-sweep (als.cpp:40-121,
-// parallel.cpp:144-185).  For every destination row c with ratings
-// {(j_t, r_t)}:
-//      (sum_t m_t m_t^T + lambda*n_c*I) u_c = sum_t r_t m_t ,  m_t = src row j_t
-// empty rows -> 0; unregularised or non-SPD systems -> least-norm solve.
-//
-// Design:
-//  * Rows are cut into segments of <= S ratings (SegPlan, heavy rows first).
-//    One group of GW warps owns a segment.  Gathered source rows are staged
-//    into shared memory with cp.async (16-byte, double-buffered, CH ratings
-//    per stage) as the augmented vector m' = [m, r] (rhs folded into the Gram).
-//  * Gram of m' on the FP64 tensor cores: mma.sync m8n8k4 f64 (SASS
-//    DMMA.8x8x4) over the NB(NB+1)/2 lower-triangular 8x8 blocks, k = 4
-//    ratings per MMA; block pairs are distributed round-robin over the warps,
-//    accumulators live in registers.
-//  * Single-segment rows finish in the same CTA: the Gram goes to shared
-//    memory, lambda*n_c is added to the diagonal and an in-place symmetric
-//    elimination (LDL^T form of Cholesky: a pivot <= 0 means "not SPD", as
-//    Eigen's LLT) runs on the augmented matrix, so the forward substitution
-//    falls out of the rhs row; one warp back-substitutes.
-//  * Multi-segment (heavy) rows write register partials per segment; a
-//    second kernel sums them in segment order (deterministic) and solves.
-//  * Fallback columns (lambda*n_c == 0 or a non-positive pivot) are listed
-//    and solved by k_hs_fallback: exact reference-order Gram, cyclic Jacobi
-//    eigen-decomposition, pseudo-inverse solve + one refinement step
-//    (als.cpp:71-81 semantics).
-#include "common.cuh"
+// k_halfsweep.cu -- K1-K4 dispatcher: picks the per-NB Gram/solve unit
+// (k_hs_inst.cu) for the rank and runs the least-norm fallback pass
+// (als.cpp:71-81) for the rows those kernels listed.
+#include "k_halfsweep.cuh"
 
 namespace ab2 {
 
+using hs::HsArgs;
+
 namespace {
-
-// One dynamic shared-memory array for every kernel of this file; all shared
-// accesses index it with 32-bit offsets so they compile to LDS/STS.
-extern __shared__ __align__(16) double g_smem[];
-
-struct HsArgs {
-  const int64_t* ptr;
-  const int* idx;
-  const double* val;
-  int row0;            // flat-vector row of local row 0 (output side)
-  const double* src;   // flat-vector row 0 of the source side
-  double* out;         // flat vector base (rows indexed by row0 + local row)
-  int n_f, ld;
-  double lambda;
-  const int* seg_row;
-  const int64_t* seg_beg;
-  const int* seg_len;
-  const int* seg_slot;
-  int n_seg;
-  const int* m_row;
-  const int* m_slot0;
-  const int* m_nslot;
-  int n_multi;
-  double* partial;
-  int* fb_list;
-  unsigned* fb_count;
-  unsigned* fb_total;
-};
-
-template <int NB, int GW>
-struct HsCfg {
-  static constexpr int P = NB * (NB + 1) / 2;     // lower-triangular block pairs
-  static constexpr int Q = (P + GW - 1) / GW;     // pairs per warp
-  static constexpr int LDS = NB * 8 + 4;          // stage row stride (bank-conflict free)
-  static constexpr int CH = GW == 1 ? 16 : 32;    // ratings per stage
-  static constexpr bool PACKED = NB > 16;
-  static constexpr int MAXF = NB * 8;
-  static constexpr int GPC = GW == 1 ? 4 : 1;     // groups per CTA
-  static constexpr int THREADS = GW * 32 * GPC;
-  static constexpr int GT = GW * 32;              // threads per group
-  static constexpr int PART = GW * Q * 64;        // doubles per partial slot
-};
-
-template <int GW>
-__device__ __forceinline__ void group_sync() {
-  if constexpr (GW == 1)
-    __syncwarp();
-  else
-    __syncthreads();
-}
-
-template <int NB, int GW>
-__host__ __device__ constexpr size_t hs_group_doubles(int ld) {
-  using C = HsCfg<NB, GW>;
-  const size_t stage = static_cast<size_t>(2) * C::CH * C::LDS;
-  const int lda = (ld + 1) | 1;
-  const size_t mat = C::PACKED ? static_cast<size_t>(ld + 1) * (ld + 2) / 2
-                               : static_cast<size_t>(ld + 1) * lda;
-  const size_t body = stage > mat ? stage : mat;
-  return body + 2 * static_cast<size_t>(C::MAXF);  // + dinv[], w[]
-}
-
-template <bool PACKED>
-__device__ __forceinline__ int midx(int i, int j, int lda) {
-  if constexpr (PACKED)
-    return i * (i + 1) / 2 + j;
-  else
-    return i * lda + j;
-}
-
-// Pair index p -> (I, J) with J <= I, row-major over the lower triangle.
-__device__ __forceinline__ void pair_ij(int p, int& I, int& J) {
-  int i = static_cast<int>((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
-  while ((i + 1) * (i + 2) / 2 <= p) ++i;
-  while (i * (i + 1) / 2 > p) --i;
-  I = i;
-  J = p - i * (i + 1) / 2;
-}
-
-// Gram of the augmented rows over one segment, accumulated into acc.
-// sb: offset (in doubles) of the group's region in g_smem.
-template <int NB, int GW>
-__device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t beg, int len,
-                                             int gtid, int warp, int lane,
-                                             double (&acc)[HsCfg<NB, GW>::Q][2],
-                                             const int (&pI)[HsCfg<NB, GW>::Q],
-                                             const int (&pJ)[HsCfg<NB, GW>::Q]) {
-  using C = HsCfg<NB, GW>;
-  constexpr int BUF = C::CH * C::LDS;
-  const int ld = a.ld;
-  const int nch = ld >> 1;  // 16-byte chunks per source row
-  const int padw = C::LDS - ld;
-  // zero the pad columns (ld .. LDS) of both buffers once; column ld carries r
-  for (int e = gtid; e < 2 * C::CH * padw; e += C::GT) {
-    const int t = e / padw, c = e - t * padw;  // t indexes rows of both buffers
-    g_smem[sb + t * C::LDS + ld + c] = 0.0;
-  }
-  group_sync<GW>();
-  // Each warp loads the stage's CH indices with one coalesced load (lane t
-  // holds rating t) and hands them out by shuffle, so every cp.async of the
-  // stage issues after a single index-load latency.
-  auto issue = [&](int s, int bo) {
-    const int base = s * C::CH;
-    const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
-    for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
-      const int c = c0 + gtid;
-      const int t = min(c / nch, C::CH - 1), k = c - t * nch;
-      const int j = __shfl_sync(kFull, jv, t);
-      if (c < C::CH * nch) {
-        double* dst = &g_smem[bo + t * C::LDS + 2 * k];
-        if (base + t < len)
-          cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
-        else
-          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
-      }
-    }
-    for (int t = gtid; t < C::CH; t += C::GT) {
-      const int rt = base + t;
-      g_smem[bo + t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
-    }
-  };
-  int aoff[C::Q], boff[C::Q];
-#pragma unroll
-  for (int q = 0; q < C::Q; ++q) {
-    aoff[q] = 8 * pI[q];
-    boff[q] = 8 * pJ[q];
-  }
-  const int lofs = (lane & 3) * C::LDS + (lane >> 2);
-  const int nst = (len + C::CH - 1) / C::CH;
-  if (nst > 0) issue(0, sb);
-  cp_async_commit();
-  for (int s = 0; s < nst; ++s) {
-    if (s + 1 < nst) {
-      issue(s + 1, sb + ((s + 1) & 1) * BUF);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    group_sync<GW>();
-    const int bo = sb + (s & 1) * BUF + lofs;
-#pragma unroll 2
-    for (int kk = 0; kk < C::CH / 4; ++kk) {
-      const int base = bo + kk * 4 * C::LDS;
-#pragma unroll
-      for (int q = 0; q < C::Q; ++q) {
-        if (q < C::Q - 1 || warp + q * GW < C::P) {
-          const double av = g_smem[base + aoff[q]];
-          const double bv = g_smem[base + boff[q]];
-          dmma884(acc[q][0], acc[q][1], av, bv);
-        }
-      }
-    }
-    group_sync<GW>();
-  }
-}
-
-// Gram (in registers) -> shared matrix -> shifted elimination -> u.
-template <int NB, int GW>
-__device__ __forceinline__ void solve_row(const HsArgs& a, double* S, int lr, int count,
-                                          int gtid, int warp, int lane,
-                                          double (&acc)[HsCfg<NB, GW>::Q][2],
-                                          const int (&pI)[HsCfg<NB, GW>::Q],
-                                          const int (&pJ)[HsCfg<NB, GW>::Q]) {
-  using C = HsCfg<NB, GW>;
-  const int n_f = a.n_f, ld = a.ld;
-  const int lda = (ld + 1) | 1;
-  double* A = S;
-  const size_t body = hs_group_doubles<NB, GW>(ld) - 2 * C::MAXF;
-  double* dinv = S + body;
-  double* w = dinv + C::MAXF;
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
-
-  group_sync<GW>();  // stage buffers are dead; A aliases them
-#pragma unroll
-  for (int q = 0; q < C::Q; ++q) {
-    if (q < C::Q - 1 || warp + q * GW < C::P) {
-      const int i = 8 * pI[q] + (lane >> 2);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = 8 * pJ[q] + 2 * (lane & 3) + e;
-        if (i <= ld && j <= i) A[midx<C::PACKED>(i, j, lda)] = acc[q][e];
-      }
-    }
-  }
-  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
-  group_sync<GW>();
-  bool ok = shift > 0.0;
-  if (ok) {
-    for (int d = gtid; d < n_f; d += C::GT) A[midx<C::PACKED>(d, d, lda)] += shift;
-    group_sync<GW>();
-    // Right-looking symmetric elimination on rows {0..n_f-1} U {ld}.
-    constexpr int TR = C::GT >= 128 ? 16 : 8;
-    constexpr int TC = C::GT / TR;
-    const int ti = gtid % TR, tj = gtid / TR;
-    for (int k = 0; k < n_f; ++k) {
-      const double d = A[midx<C::PACKED>(k, k, lda)];
-      if (!(d > 0.0)) {  // Eigen LLT reports NumericalIssue on pivot <= 0
-        ok = false;
-        break;
-      }
-      const double invd = 1.0 / d;
-      if (gtid == 0) dinv[k] = invd;
-      const int nreg = n_f - 1 - k;
-      for (int ii = ti; ii <= nreg; ii += TR) {
-        const int i = ii < nreg ? k + 1 + ii : ld;
-        const int jmax = ii < nreg ? i : n_f - 1;
-        const double s = A[midx<C::PACKED>(i, k, lda)] * invd;
-        for (int j = k + 1 + tj; j <= jmax; j += TC)
-          A[midx<C::PACKED>(i, j, lda)] =
-              fma(-s, A[midx<C::PACKED>(j, k, lda)], A[midx<C::PACKED>(i, j, lda)]);
-      }
-      group_sync<GW>();
-    }
-  }
-  if (!ok) {
-    if (gtid == 0) {
-      const unsigned slot = atomicAdd(a.fb_count, 1u);
-      a.fb_list[slot] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  // Back substitution (warp 0): u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
-  if (warp == 0) {
-    for (int i = lane; i < n_f; i += 32) w[i] = A[midx<C::PACKED>(ld, i, lda)];
-    __syncwarp();
-    for (int k = n_f - 1; k >= 0; --k) {
-      const double u = w[k] * dinv[k];
-      for (int i = lane; i < k; i += 32) w[i] = fma(-A[midx<C::PACKED>(k, i, lda)], u, w[i]);
-      if (lane == 0) out[k] = u;
-      __syncwarp();
-    }
-    if (lane == 0 && ld > n_f) out[n_f] = 0.0;
-  }
-}
-
-template <int NB, int GW>
-__device__ __forceinline__ void init_pairs(int warp, int (&pI)[HsCfg<NB, GW>::Q],
-                                           int (&pJ)[HsCfg<NB, GW>::Q],
-                                           double (&acc)[HsCfg<NB, GW>::Q][2]) {
-  using C = HsCfg<NB, GW>;
-#pragma unroll
-  for (int q = 0; q < C::Q; ++q) {
-    const int p = warp + q * GW;
-    int I = 0, J = 0;
-    if (p < C::P) pair_ij(p, I, J);
-    pI[q] = I;
-    pJ[q] = J;
-    acc[q][0] = 0.0;
-    acc[q][1] = 0.0;
-  }
-}
-
-template <int NB, int GW>
-__global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
-  using C = HsCfg<NB, GW>;
-  const int group = threadIdx.x / C::GT;
-  const int gtid = threadIdx.x % C::GT;
-  const int warp = gtid >> 5, lane = gtid & 31;
-  const int seg = blockIdx.x * C::GPC + group;
-  if (seg >= a.n_seg) return;  // uniform per group (GW==1 groups are warps)
-  const int sbase = group * static_cast<int>(hs_group_doubles<NB, GW>(a.ld));
-  double* S = g_smem + sbase;
-  const int lr = a.seg_row[seg];
-  const int len = a.seg_len[seg];
-  const int slot = a.seg_slot[seg];
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * a.ld;
-  if (len == 0) {  // zero-rating column stays zero (parallel.cpp:175)
-    for (int k = gtid; k < a.ld; k += C::GT) out[k] = 0.0;
-    return;
-  }
-  int pI[C::Q], pJ[C::Q];
-  double acc[C::Q][2];
-  init_pairs<NB, GW>(warp, pI, pJ, acc);
-  gram_segment<NB, GW>(a, sbase, a.seg_beg[seg], len, gtid, warp, lane, acc, pI, pJ);
-  if (slot >= 0) {
-    double* P = a.partial + static_cast<int64_t>(slot) * C::PART;
-#pragma unroll
-    for (int q = 0; q < C::Q; ++q)
-      *reinterpret_cast<double2*>(P + (warp * C::Q + q) * 64 + lane * 2) =
-          make_double2(acc[q][0], acc[q][1]);
-    return;
-  }
-  solve_row<NB, GW>(a, S, lr, len, gtid, warp, lane, acc, pI, pJ);
-}
-
-template <int NB, int GW>
-__global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) {
-  using C = HsCfg<NB, GW>;
-  const int group = threadIdx.x / C::GT;
-  const int gtid = threadIdx.x % C::GT;
-  const int warp = gtid >> 5, lane = gtid & 31;
-  const int m = blockIdx.x * C::GPC + group;
-  if (m >= a.n_multi) return;
-  double* S = g_smem + static_cast<size_t>(group) * hs_group_doubles<NB, GW>(a.ld);
-  int pI[C::Q], pJ[C::Q];
-  double acc[C::Q][2];
-  init_pairs<NB, GW>(warp, pI, pJ, acc);
-  const int slot0 = a.m_slot0[m], ns = a.m_nslot[m];
-  for (int s = 0; s < ns; ++s) {  // segment order -> deterministic
-    const double* P = a.partial + static_cast<int64_t>(slot0 + s) * C::PART;
-#pragma unroll
-    for (int q = 0; q < C::Q; ++q) {
-      const double2 v = *reinterpret_cast<const double2*>(P + (warp * C::Q + q) * 64 + lane * 2);
-      acc[q][0] += v.x;
-      acc[q][1] += v.y;
-    }
-  }
-  const int lr = a.m_row[m];
-  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  solve_row<NB, GW>(a, S, lr, count, gtid, warp, lane, acc, pI, pJ);
-}
-
-// ------------------------------------------------ split path (n_f >= 31) --
-// K1/K2: Gram-only kernel.  The NB(NB+1)/2 lower-triangular 8x8 blocks are
-// split into GR bands of block rows (compile-time, balanced pair counts);
-// warp w owns band w / GK and every GK-th k-step (k-group w % GK).  Per
-// k-step a warp loads each needed 8-row fragment ONCE into registers (the
-// A fragment of block I equals the B fragment of block I) and issues all of
-// its band's DMMAs from registers: ~0.3 shared loads per DMMA instead of 2,
-// which is what lets the FP64 tensor pipe run near its peak.
-constexpr int kGramStage = 32;  // ratings per TMA stage in the Gram kernel
-
-template <int NB>
-struct GramShape {
-  static constexpr int P = NB * (NB + 1) / 2;
-  // ~24 block pairs per warp (48 accumulator doubles): enough register reuse
-  // per fragment load, and light enough for 3-4 CTAs per SM.
-  // <= ~48 block pairs (96 accumulator doubles) per warp; the k-steps of a
-  // stage are split over GK warps per band when there are few bands.
-  static constexpr int GR = (P + 47) / 48 < 2 ? 2 : ((P + 47) / 48 > 8 ? 8 : (P + 47) / 48);
-  static constexpr int GK = GR >= 4 ? 1 : 4 / GR;
-  static constexpr int W = GR * GK;
-  // first block row of band r (balanced by pair count)
-  static constexpr int band_start(int r) {
-    if (r <= 0) return 0;
-    if (r >= GR) return NB;
-    int acc = 0;
-    for (int I = 0; I < NB; ++I) {
-      if (acc * GR >= r * P) return I;
-      acc += I + 1;
-    }
-    return NB;
-  }
-  static constexpr int band_pairs(int r) {
-    const int a = band_start(r), b = band_start(r + 1);
-    return b * (b + 1) / 2 - a * (a + 1) / 2;
-  }
-  static constexpr int max_pairs() {
-    int m = 0;
-    for (int r = 0; r < GR; ++r) m = band_pairs(r) > m ? band_pairs(r) : m;
-    return m;
-  }
-  static constexpr int MAXP = max_pairs();
-};
-
-template <int NB, int R>
-__device__ __forceinline__ void gram_band_kstep(int base, double (&acc)[GramShape<NB>::MAXP][2]) {
-  using G = GramShape<NB>;
-  constexpr int I0 = G::band_start(R), I1 = G::band_start(R + 1);
-  double f[I1 > 0 ? I1 : 1];
-#pragma unroll
-  for (int b = 0; b < I1; ++b) f[b] = g_smem[base + 8 * b];
-  int p = 0;
-#pragma unroll
-  for (int I = I0; I < I1; ++I)
-#pragma unroll
-    for (int J = 0; J <= I; ++J) {
-      dmma884(acc[p][0], acc[p][1], f[I], f[J]);
-      ++p;
-    }
-}
-
-template <int NB, int R>
-__device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len, int kgroup,
-                                          int lane, double (&acc)[GramShape<NB>::MAXP][2]) {
-  using G = GramShape<NB>;
-  using C = HsCfg<NB, G::W>;
-  constexpr int CH = kGramStage;
-  constexpr int BUF = CH * C::LDS;
-  const int gtid = threadIdx.x, warp = gtid >> 5;
-  const int ld = a.ld;
-  const int padw = C::LDS - ld;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + 2 * BUF);  // 2 mbarriers after the buffers
-  for (int e = gtid; e < 2 * CH * padw; e += C::GT) {
-    const int t = e / padw, c = e - t * padw;
-    g_smem[t * C::LDS + ld + c] = 0.0;
-  }
-  if (gtid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  // Stage s -> buffer s&1: warp 0 gathers the stage's rows with one TMA bulk
-  // copy per rating (lane t copies source row idx[t], ld*8 bytes) completing
-  // on the buffer's mbarrier; missing tail rows are zero-filled and the
-  // rating values go to column ld with ordinary stores.
-  auto issue = [&](int s) {
-    const int base = s * CH;
-    const int bo = (s & 1) * BUF;
-    const int nv = min(CH, len - base);
-    if (warp == 0) {
-      fence_proxy_async_smem();  // prior generic reads of this buffer happen-before the async writes
-      if (lane == 0) mbar_arrive_expect_tx(bar + (s & 1), static_cast<unsigned>(nv) * ld * 8);
-      __syncwarp();
-      for (int t = lane; t < nv; t += 32) {
-        const int j = a.idx[beg + base + t];
-        tma_load_1d(&g_smem[bo + t * C::LDS], a.src + static_cast<int64_t>(j) * ld,
-                    static_cast<unsigned>(ld) * 8, bar + (s & 1));
-      }
-    }
-    for (int e = gtid; e < (CH - nv) * ld; e += C::GT) {
-      const int t = nv + e / ld, c = e % ld;
-      g_smem[bo + t * C::LDS + c] = 0.0;
-    }
-    for (int t = gtid; t < CH; t += C::GT)
-      g_smem[bo + t * C::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
-  };
-  const int lofs = (lane & 3) * C::LDS + (lane >> 2);
-  const int nst = (len + CH - 1) / CH;
-  if (nst > 0) issue(0);
-  for (int s = 0; s < nst; ++s) {
-    if (s + 1 < nst) issue(s + 1);
-    mbar_wait(bar + (s & 1), (s >> 1) & 1);
-    __syncthreads();  // zero rows / rating column of stage s visible
-    const int bo = (s & 1) * BUF + lofs;
-#pragma unroll
-    for (int kk = kgroup; kk < CH / 4; kk += G::GK) gram_band_kstep<NB, R>(bo + kk * 4 * C::LDS, acc);
-    __syncthreads();
-  }
-}
-
-template <int NB, int R>
-__device__ __forceinline__ void gram_band_out(int kgroup, int lane, double* out,
-                                              double (&acc)[GramShape<NB>::MAXP][2]) {
-  using G = GramShape<NB>;
-  constexpr int I0 = G::band_start(R);
-  constexpr int NP = G::band_pairs(R);
-  constexpr int p0 = I0 * (I0 + 1) / 2;
-  // k-groups > 0 park their partials in shared memory; k-group 0 adds them in
-  // k-group order (deterministic) and writes the band's canonical blocks.
-  double* park = g_smem + R * (G::GK - 1) * G::MAXP * 64;
-  if (kgroup > 0) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-      *reinterpret_cast<double2*>(park + ((kgroup - 1) * G::MAXP + p) * 64 + lane * 2) =
-          make_double2(acc[p][0], acc[p][1]);
-  }
-  __syncthreads();
-  if (kgroup == 0) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      double2 v = make_double2(acc[p][0], acc[p][1]);
-      for (int g = 1; g < G::GK; ++g) {
-        const double2 u = *reinterpret_cast<const double2*>(park + ((g - 1) * G::MAXP + p) * 64 + lane * 2);
-        v.x += u.x;
-        v.y += u.y;
-      }
-      __stcs(reinterpret_cast<double2*>(out + (p0 + p) * 64 + lane * 2), v);  // streaming: keep L2 for factor rows
-    }
-  }
-}
-
-template <int NB>
-__global__ void __launch_bounds__(GramShape<NB>::W * 32)
-    k_hs_gram(HsArgs a, const int* __restrict__ seg_len, const int64_t* __restrict__ seg_beg,
-              const int* __restrict__ seg_slot, double* __restrict__ G) {
-  using GS = GramShape<NB>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int band = warp / GS::GK, kgroup = warp % GS::GK;
-  const int seg = blockIdx.x;
-  const int64_t beg = seg_beg[seg];
-  const int len = seg_len[seg];
-  double* out = G + static_cast<int64_t>(seg_slot[seg]) * GS::P * 64;
-  double acc[GS::MAXP][2];
-#pragma unroll
-  for (int p = 0; p < GS::MAXP; ++p) acc[p][0] = acc[p][1] = 0.0;
-  // one fully specialised body per band (compile-time fragment indices)
-#define AB2_BAND(R)                                              \
-  if (band == R && R < GS::GR) {                                 \
-    gram_band<NB, (R < GS::GR ? R : 0)>(a, beg, len, kgroup, lane, acc); \
-    gram_band_out<NB, (R < GS::GR ? R : 0)>(kgroup, lane, out, acc);     \
-  }
-  AB2_BAND(0) AB2_BAND(1) AB2_BAND(2) AB2_BAND(3) AB2_BAND(4) AB2_BAND(5) AB2_BAND(6) AB2_BAND(7)
-  AB2_BAND(8) AB2_BAND(9) AB2_BAND(10) AB2_BAND(11) AB2_BAND(12) AB2_BAND(13) AB2_BAND(14) AB2_BAND(15)
-#undef AB2_BAND
-}
-
-// Warp-specialised persistent Gram kernel (the split path's K1/K2).
-//  * warp GR is the producer: for every stage of every segment this CTA owns
-//    it waits for the ring slot to be released, writes the rating column and
-//    zero tail rows, then gathers the stage's source rows with one TMA bulk
-//    copy per rating (cp.async.bulk ... mbarrier::complete_tx);
-//  * warps 0..GR-1 are consumers: warp r owns the compile-time contiguous
-//    range of canonical block pairs [r*P/GR, (r+1)*P/GR), loads each needed
-//    8-row fragment once per k-step and issues its DMMAs from registers; it
-//    releases the slot with an mbarrier arrive.  No CTA-wide barrier in the
-//    main loop; the producer runs ahead across segment boundaries.
-constexpr int kWsStages = 3;
-constexpr int kWsCH = 32;
-
-template <int NB>
-struct WsShape {
-  static constexpr int P = NB * (NB + 1) / 2;
-  // ~12 block pairs per consumer warp, 2..8 consumers
-  static constexpr int GR = P < 2 ? 1 : ((P + 11) / 12 < 2 ? 2 : ((P + 11) / 12 > 8 ? 8 : (P + 11) / 12));
-  static constexpr int LDS = NB * 8 + 4;
-  static constexpr int BUF = kWsCH * LDS;
-  static constexpr int p_begin(int r) { return r * P / GR; }
-  static constexpr int row_of(int p) {
-    int i = 0;
-    while ((i + 1) * (i + 2) / 2 <= p) ++i;
-    return i;
-  }
-  static constexpr int col_of(int p) { return p - row_of(p) * (row_of(p) + 1) / 2; }
-  static constexpr bool needs(int r, int b) {
-    for (int p = p_begin(r); p < p_begin(r + 1); ++p)
-      if (row_of(p) == b || col_of(p) == b) return true;
-    return false;
-  }
-  static constexpr int max_pairs() {
-    int m = 0;
-    for (int r = 0; r < GR; ++r) m = p_begin(r + 1) - p_begin(r) > m ? p_begin(r + 1) - p_begin(r) : m;
-    return m;
-  }
-  static constexpr int MAXP = max_pairs();
-  static constexpr size_t smem_bytes() {
-    return sizeof(double) * kWsStages * BUF + 2 * kWsStages * sizeof(uint64_t);
-  }
-};
-
-template <int NB, int R>
-__device__ __forceinline__ void ws_kstep(int base, double (&acc)[WsShape<NB>::MAXP][2]) {
-  using S = WsShape<NB>;
-  constexpr int p0 = S::p_begin(R), p1 = S::p_begin(R + 1);
-  double f[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b)
-    if (S::needs(R, b)) f[b] = g_smem[base + 8 * b];
-#pragma unroll
-  for (int p = p0; p < p1; ++p)
-    dmma884(acc[p - p0][0], acc[p - p0][1], f[S::row_of(p)], f[S::col_of(p)]);
-}
-
-template <int NB, int R>
-__device__ __forceinline__ void ws_consumer(const int* __restrict__ seg_len,
-                                            const int* __restrict__ seg_slot, int n_seg,
-                                            double* __restrict__ G, uint64_t* full,
-                                            uint64_t* empty, int lane) {
-  using S = WsShape<NB>;
-  constexpr int p0 = S::p_begin(R), np = S::p_begin(R + 1) - p0;
-  const int lofs = (lane & 3) * S::LDS + (lane >> 2);
-  int it = 0;
-  for (int seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
-    double acc[S::MAXP][2];
-#pragma unroll
-    for (int p = 0; p < S::MAXP; ++p) acc[p][0] = acc[p][1] = 0.0;
-    const int nst = (seg_len[seg] + kWsCH - 1) / kWsCH;
-    for (int s = 0; s < nst; ++s, ++it) {
-      const int buf = it % kWsStages;
-      mbar_wait(full + buf, (it / kWsStages) & 1);
-      const int bo = buf * S::BUF + lofs;
-#pragma unroll
-      for (int kk = 0; kk < kWsCH / 4; ++kk) ws_kstep<NB, R>(bo + kk * 4 * S::LDS, acc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + buf);
-    }
-    double* out = G + static_cast<int64_t>(seg_slot[seg]) * S::P * 64 + p0 * 64 + lane * 2;
-#pragma unroll
-    for (int p = 0; p < np; ++p)
-      __stcs(reinterpret_cast<double2*>(out + p * 64), make_double2(acc[p][0], acc[p][1]));
-  }
-}
-
-template <int NB>
-__global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
-    k_hs_gram_ws(HsArgs a, const int* __restrict__ seg_len, const int64_t* __restrict__ seg_beg,
-                 const int* __restrict__ seg_slot, int n_seg, double* __restrict__ G) {
-  using S = WsShape<NB>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ld = a.ld;
-  uint64_t* full = reinterpret_cast<uint64_t*>(g_smem + kWsStages * S::BUF);
-  uint64_t* empty = full + kWsStages;
-  // pad columns ld+1 .. LDS-1 stay zero for the whole kernel
-  const int padw = S::LDS - ld - 1;
-  for (int e = threadIdx.x; e < kWsStages * kWsCH * padw; e += blockDim.x) {
-    const int t = e / padw, c = e - t * padw;
-    g_smem[t * S::LDS + ld + 1 + c] = 0.0;
-  }
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kWsStages; ++i) {
-      mbar_init(full + i, 1);
-      mbar_init(empty + i, S::GR);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (warp == S::GR) {  // ---------------- producer
-    int it = 0;
-    for (int seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
-      const int len = seg_len[seg];
-      const int64_t beg = seg_beg[seg];
-      for (int base = 0; base < len; base += kWsCH, ++it) {
-        const int buf = it % kWsStages, use = it / kWsStages;
-        if (use > 0) mbar_wait(empty + buf, (use - 1) & 1);
-        double* B = g_smem + buf * S::BUF;
-        const int nv = min(kWsCH, len - base);
-        const int t = lane;  // kWsCH == 32: one rating per lane
-        B[t * S::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
-        if (t >= nv)
-          for (int c = 0; c < ld; c += 2) *reinterpret_cast<double2*>(B + t * S::LDS + c) = make_double2(0.0, 0.0);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(full + buf, static_cast<unsigned>(nv) * ld * 8);
-        if (t < nv)
-          tma_load_1d(B + t * S::LDS, a.src + static_cast<int64_t>(a.idx[beg + base + t]) * ld,
-                      static_cast<unsigned>(ld) * 8, full + buf);
-      }
-    }
-    return;
-  }
-  // ------------------------------------------ consumers (compile-time band)
-#define AB2_WS(R)                                                                           \
-  if (warp == R && R < S::GR)                                                               \
-    ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, lane);
-  AB2_WS(0) AB2_WS(1) AB2_WS(2) AB2_WS(3) AB2_WS(4) AB2_WS(5) AB2_WS(6) AB2_WS(7)
-#undef AB2_WS
-}
-
-struct SolveArgs {
-  int row0;     // first local row of the batch
-  int nrows;    // rows in the batch
-  const int* row_slot0;
-  const int* row_nslot;
-  const double* G;
-};
-
-template <int NB>
-struct SolveCfg {
-  static constexpr int P = NB * (NB + 1) / 2;
-  static constexpr int PER_WARP = P * 64 + 2 * NB * 8;  // doubles: blocks + dinv + w
-  static constexpr int FIT = (220 * 1024) / (PER_WARP * 8);
-  static constexpr int WPB = FIT >= 8 ? 8 : (FIT < 1 ? 1 : FIT);
-};
-
-__device__ __forceinline__ int pidx(int I, int J) { return I * (I + 1) / 2 + J; }
-// Swizzled 8x8 block storage: element (r, c) at 8r + (c ^ 4*((r>>1)&1)); the
-// C-fragment (16-byte) and A/B-fragment (8-byte) accesses are conflict-free.
-__device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r >> 1) & 1))); }
-
-// K3: batched solve.  One warp per column: sums the column's partial Grams
-// (slot order) into a swizzled shared copy, adds lambda*n_c, then a
-// left-looking blocked LDL^T over 8-column block columns J:
-//   (1) C(I,J) -= sum_{K<J} L(I,K) * (D_K^-1 L(J,K))^T on the FP64 tensor
-//       cores, two block rows at a time (independent DMMA chains);
-//   (2) the 8x8 diagonal block is factored by lanes 0..7 (one row each);
-//   (3) the rows below are eliminated lane-parallel (TRSM form, 28 FMAs per
-//       row against the factored diagonal block).
-// Storage is unscaled (A(i,k) = L~(i,k) d_k) so the augmented rhs row is
-// eliminated with the matrix and forward substitution comes for free.
-template <int NB>
-__device__ __forceinline__ bool ldl_factor(double* M, double* dinv, int n_f, int lane) {
-  const int r = lane >> 2, q = lane & 3;
-  const int KP = (n_f + 7) / 8;
-  for (int J = 0; J < KP; ++J) {
-    // (1) updates from earlier panels, four block rows per pass (four
-    // independent DMMA accumulation chains)
-    if (J > 0) {
-      const double* bj = M + pidx(J, 0) * 64;
-      for (int I = J; I < NB; I += 4) {
-        double2 c[4];
-        const double* ap[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int Iu = min(I + u, NB - 1);
-          c[u] = *reinterpret_cast<const double2*>(M + pidx(Iu, J) * 64 + swz(r, 2 * q));
-          ap[u] = M + pidx(Iu, 0) * 64;
-        }
-        for (int K = 0; K < J; ++K) {
-          const int o = K * 64;
-          const double b0 = bj[o + swz(r, q)] * dinv[8 * K + q];
-          const double b1 = bj[o + swz(r, 4 + q)] * dinv[8 * K + 4 + q];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dmma884(c[u].x, c[u].y, -ap[u][o + swz(r, q)], b0);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dmma884(c[u].x, c[u].y, -ap[u][o + swz(r, 4 + q)], b1);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (I + u < NB) *reinterpret_cast<double2*>(M + pidx(I + u, J) * 64 + swz(r, 2 * q)) = c[u];
-      }
-      __syncwarp();
-    }
-    // (2) diagonal block: lane rr < 8 holds row rr of block (J,J)
-    double* D = M + pidx(J, J) * 64;
-    const int rr = lane & 7;
-    double row[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int k = 8 * J + c;
-      if (k >= n_f) {  // non-pivot columns (padding / rhs column)
-        if (lane == 0) dinv[k] = 0.0;
-        continue;
-      }
-      const double d = __shfl_sync(kFull, row[c], c);
-      if (!(d > 0.0)) return false;  // Eigen LLT: NumericalIssue on a non-positive pivot
-      const double inv = fast_rcp(d);
-      if (lane == 0) dinv[k] = inv;
-      const double l = row[c] * inv;
-#pragma unroll
-      for (int c2 = c + 1; c2 < 8; ++c2) {
-        const double a = __shfl_sync(kFull, row[c], c2);  // A(c2, c)
-        if (rr > c && c2 <= rr) row[c2] = fma(-l, a, row[c2]);
-      }
-    }
-    if (lane < 8)
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c <= rr) D[swz(rr, c)] = row[c];
-    __syncwarp();
-    // (3) rows below the diagonal block: x_c' -= x_c * A(c',c)/d_c
-    if (J + 1 < NB) {
-      double s[28];
-      {
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) s[t++] = D[swz(c2, c)] * dinv[8 * J + c];
-      }
-      for (int i = 8 * (J + 1) + lane; i < 8 * NB; i += 32) {
-        double* rowp = M + pidx(i >> 3, J) * 64;
-        const int ri = i & 7;
-        double x[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) x[c] = rowp[swz(ri, c)];
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], s[t++], x[c2]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) rowp[swz(ri, c)] = x[c];
-      }
-      __syncwarp();
-    }
-  }
-  return true;
-}
-
-template <int NB>
-__global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
-    k_hs_solve(HsArgs a, SolveArgs s) {
-  using C = SolveCfg<NB>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rl = blockIdx.x * C::WPB + warp;
-  if (rl >= s.nrows) return;
-  const int lr = s.row0 + rl;
-  const int n_f = a.n_f, ld = a.ld;
-  double* M = g_smem + static_cast<size_t>(warp) * C::PER_WARP;
-  double* dinv = M + C::P * 64;
-  double* w = dinv + NB * 8;
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
-  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
-    for (int k = lane; k < ld; k += 32) out[k] = 0.0;
-    return;
-  }
-  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
-  if (!(shift > 0.0)) {
-    if (lane == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int r = lane >> 2, q = lane & 3;
-  {
-    const int ns = s.row_nslot[lr];
-    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
-    if (ns == 1) {
-      // one slot: bulk 16-byte async copies straight into the swizzled blocks
-#pragma unroll 8
-      for (int p = 0; p < C::P; ++p) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
-      cp_async_commit();
-      cp_async_wait<0>();
-    } else {
-      for (int p = 0; p < C::P; ++p) {  // heavy rows: sum slots in slot order
-        double2 v = *reinterpret_cast<const double2*>(base + p * 64);
-        for (int t = 1; t < ns; ++t) {
-          const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
-          v.x += u.x;
-          v.y += u.y;
-        }
-        *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
-      }
-    }
-    __syncwarp();
-    // lambda * n_c on the diagonal (als.cpp:58-59): lane (r, q) owns (r, 2q+e)
-#pragma unroll
-    for (int I = 0; I < NB; ++I)
-      if (8 * I + r < n_f && (r >> 1) == q) M[pidx(I, I) * 64 + swz(r, r)] += shift;
-  }
-  __syncwarp();
-  if (!ldl_factor<NB>(M, dinv, n_f, lane)) {
-    if (lane == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int KP = (n_f + 7) / 8;
-  // Back substitution: u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k, one
-  // 8-row panel at a time: the panel's 8 unknowns by shuffles in lanes 0..7,
-  // then every lane folds them into the remaining right-hand side.
-  const int IR = ld >> 3, rr = ld & 7;
-  for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
-  __syncwarp();
-  for (int K = KP - 1; K >= 0; --K) {
-    const int kc = 8 * K + (lane & 7);
-    double wk = (lane < 8 && kc < n_f) ? w[kc] : 0.0;
-    const double dk = (lane < 8 && kc < n_f) ? dinv[kc] : 0.0;
-#pragma unroll
-    for (int c = 7; c >= 0; --c) {
-      const double u = __shfl_sync(kFull, wk * dk, c);
-      if (lane < c) wk = fma(-M[pidx(K, K) * 64 + swz(c, lane)], u, wk);
-      if (lane == c) wk = u;
-    }
-    if (lane < 8 && kc < n_f) w[kc] = wk;
-    double uu[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) uu[c] = __shfl_sync(kFull, wk, c);
-    for (int i = lane; i < 8 * K; i += 32) {
-      const double* blk = M + pidx(K, i >> 3) * 64;
-      double acc = w[i];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (8 * K + c < n_f) acc = fma(-blk[swz(c, i & 7)], uu[c], acc);
-      w[i] = acc;
-    }
-    __syncwarp();
-  }
-  for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
-}
-
-// K3 (CTA form): one 4-warp CTA per column, right-looking blocked LDL^T.
-// Per 8-column panel J: (a) lanes 0..7 of warp 0 factor the diagonal block,
-// (b) all threads eliminate the panel rows below it (TRSM form), (c) the
-// four warps apply the panel to the trailing blocks with DMMA
-// (C(I,K) -= L(I,J) (D_J^-1 L(K,J))^T).  Back substitution by warp 0.
-constexpr int kSolveCtaWarps = 4;
-
-template <int NB>
-__global__ void __launch_bounds__(kSolveCtaWarps * 32) k_hs_solve_cta(HsArgs a, SolveArgs s) {
-  using C = SolveCfg<NB>;
-  constexpr int NT = kSolveCtaWarps * 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int lr = s.row0 + blockIdx.x;
-  const int n_f = a.n_f, ld = a.ld;
-  double* M = g_smem;
-  double* dinv = M + C::P * 64;
-  double* w = dinv + NB * 8;
-  __shared__ int fail;
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
-  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  if (count == 0) {
-    for (int k = tid; k < ld; k += NT) out[k] = 0.0;
-    return;
-  }
-  const double shift = a.lambda * static_cast<double>(count);
-  if (!(shift > 0.0)) {
-    if (tid == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int r = lane >> 2, q = lane & 3;
-  {
-    const int ns = s.row_nslot[lr];
-    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
-    if (ns == 1) {
-      for (int p = warp; p < C::P; p += kSolveCtaWarps) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
-      cp_async_commit();
-      cp_async_wait<0>();
-    } else {
-      for (int p = warp; p < C::P; p += kSolveCtaWarps) {
-        double2 v = *reinterpret_cast<const double2*>(base + p * 64);
-        for (int t = 1; t < ns; ++t) {
-          const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
-          v.x += u.x;
-          v.y += u.y;
-        }
-        *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
-      }
-    }
-    if (tid == 0) fail = 0;
-    __syncthreads();
-    for (int k = tid; k < n_f; k += NT) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;
-    __syncthreads();
-  }
-  const int KP = (n_f + 7) / 8;
-  for (int J = 0; J < KP; ++J) {
-    double* D = M + pidx(J, J) * 64;
-    // (a) diagonal block
-    if (warp == 0) {
-      const int rr = lane & 7;
-      double row[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
-      bool ok = true;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int k = 8 * J + c;
-        if (k >= n_f) {
-          if (lane == 0) dinv[k] = 0.0;
-          continue;
-        }
-        const double d = __shfl_sync(kFull, row[c], c);
-        if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
-          ok = false;
-          break;
-        }
-        const double inv = fast_rcp(d);
-        if (lane == 0) dinv[k] = inv;
-        const double l = row[c] * inv;
-#pragma unroll
-        for (int c2 = c + 1; c2 < 8; ++c2) {
-          const double av = __shfl_sync(kFull, row[c], c2);
-          if (rr > c && c2 <= rr) row[c2] = fma(-l, av, row[c2]);
-        }
-      }
-      if (!ok) {
-        if (lane == 0) fail = 1;
-      } else if (lane < 8) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c <= rr) D[swz(rr, c)] = row[c];
-      }
-    }
-    __syncthreads();
-    if (fail) break;
-    // (b) rows below the diagonal block
-    if (J + 1 < NB) {
-      double sc[28];
-      {
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) sc[t++] = D[swz(c2, c)] * dinv[8 * J + c];
-      }
-      for (int i = 8 * (J + 1) + tid; i < 8 * NB; i += NT) {
-        double* rowp = M + pidx(i >> 3, J) * 64;
-        const int ri = i & 7;
-        double x[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) x[c] = rowp[swz(ri, c)];
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], sc[t++], x[c2]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) rowp[swz(ri, c)] = x[c];
-      }
-    }
-    __syncthreads();
-    // (c) trailing update by panel J: block columns Kc in (J, KP), rows I in [Kc, NB)
-    if (J + 1 < KP) {
-      const double dk0 = dinv[8 * J + q], dk1 = dinv[8 * J + 4 + q];
-      for (int Kc = J + 1; Kc < KP; ++Kc) {
-        const double* bk = M + pidx(Kc, J) * 64;
-        const double b0 = bk[swz(r, q)] * dk0, b1 = bk[swz(r, 4 + q)] * dk1;
-        for (int I = Kc + warp; I < NB; I += 2 * kSolveCtaWarps) {
-          const int I2 = I + kSolveCtaWarps;
-          const bool two = I2 < NB;
-          const double* a0 = M + pidx(I, J) * 64;
-          const double* a1 = M + pidx(two ? I2 : I, J) * 64;
-          double* c0p = M + pidx(I, Kc) * 64 + swz(r, 2 * q);
-          double* c1p = M + pidx(two ? I2 : I, Kc) * 64 + swz(r, 2 * q);
-          double2 c0 = *reinterpret_cast<const double2*>(c0p);
-          double2 c1 = *reinterpret_cast<const double2*>(c1p);
-          dmma884(c0.x, c0.y, -a0[swz(r, q)], b0);
-          dmma884(c1.x, c1.y, -a1[swz(r, q)], b0);
-          dmma884(c0.x, c0.y, -a0[swz(r, 4 + q)], b1);
-          dmma884(c1.x, c1.y, -a1[swz(r, 4 + q)], b1);
-          *reinterpret_cast<double2*>(c0p) = c0;
-          if (two) *reinterpret_cast<double2*>(c1p) = c1;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (fail) {
-    if (tid == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  if (warp != 0) return;
-  // Back substitution (warp 0): u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
-  const int IR = ld >> 3, rr = ld & 7;
-  for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
-  __syncwarp();
-  for (int K = KP - 1; K >= 0; --K) {
-    const int kc = 8 * K + (lane & 7);
-    double wk = (lane < 8 && kc < n_f) ? w[kc] : 0.0;
-    const double dk = (lane < 8 && kc < n_f) ? dinv[kc] : 0.0;
-#pragma unroll
-    for (int c = 7; c >= 0; --c) {
-      const double u = __shfl_sync(kFull, wk * dk, c);
-      if (lane < c) wk = fma(-M[pidx(K, K) * 64 + swz(c, lane)], u, wk);
-      if (lane == c) wk = u;
-    }
-    if (lane < 8 && kc < n_f) w[kc] = wk;
-    double uu[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) uu[c] = __shfl_sync(kFull, wk, c);
-    for (int i = lane; i < 8 * K; i += 32) {
-      const double* blk = M + pidx(K, i >> 3) * 64;
-      double acc = w[i];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (8 * K + c < n_f) acc = fma(-blk[swz(c, i & 7)], uu[c], acc);
-      w[i] = acc;
-    }
-    __syncwarp();
-  }
-  for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
-}
 
 // ------------------------------------------------------------ fallback --
 // Least-norm solve for listed rows.  Workspace per CTA: W (n x n), Q (n x n).
@@ -1237,112 +180,6 @@ __global__ void __launch_bounds__(kFbThreads) k_hs_fallback(HsArgs a, double* wo
   }
 }
 
-template <int NB>
-struct Mode {
-  static constexpr int GW = NB <= 4 ? 1 : (NB <= 16 ? 4 : (NB <= 20 ? 8 : 16));
-};
-
-constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
-constexpr bool kSolveCta = true;                  // CTA-per-column solve for n_f >= 63
-
-template <int NB>
-void run_hs(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
-  constexpr int GW = Mode<NB>::GW;
-  using C = HsCfg<NB, GW>;
-  if constexpr (NB <= 4) {
-    // fused warp-per-segment kernel (Gram + solve in one pass)
-    const SegPlan& P = R.plan(kind, S);
-    a.seg_row = P.seg_row;
-    a.seg_beg = P.seg_beg;
-    a.seg_len = P.seg_len;
-    a.seg_slot = P.seg_slot;
-    a.n_seg = P.n_seg;
-    a.m_row = P.m_row;
-    a.m_slot0 = P.m_slot0;
-    a.m_nslot = P.m_nslot;
-    a.n_multi = P.n_multi;
-    const size_t smem = sizeof(double) * hs_group_doubles<NB, GW>(a.ld) * C::GPC;
-    static bool attr_set = false;
-    if (!attr_set) {
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_main<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_reduce<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr_set = true;
-    }
-    if (P.n_slots > 0)
-      a.partial = static_cast<double*>(ctx->scratch(2, sizeof(double) * C::PART * P.n_slots));
-    {
-      const int blocks = (P.n_seg + C::GPC - 1) / C::GPC;
-      const int tok = ctx->begin_launch("halfsweep_fused");
-      k_hs_main<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
-      ctx->end_launch(tok);
-    }
-    if (P.n_multi > 0) {
-      const int blocks = (P.n_multi + C::GPC - 1) / C::GPC;
-      const int tok = ctx->begin_launch("halfsweep_fused_reduce");
-      k_hs_reduce<NB, GW><<<blocks, C::THREADS, smem, ctx->stream>>>(a);
-      ctx->end_launch(tok);
-    }
-  } else {
-    using SC = SolveCfg<NB>;
-    const size_t slot_bytes = sizeof(double) * C::P * 64;
-    const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
-    using GS = GramShape<NB>;
-    using GC = HsCfg<NB, GS::W>;
-    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * kGramStage * GC::LDS + 2,
-                                                           size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
-    const size_t ssmem = sizeof(double) * SC::PER_WARP * SC::WPB;
-    static bool attr_set = false;
-    if (!attr_set) {
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_cta<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr_set = true;
-    }
-    double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
-    // Keep the gathered source factor rows resident in L2 while the Gram
-    // stream (written with evict-first stores) passes through.
-    const int n_src = kind == 0 ? R.n_m : R.n_u;
-    L2Window l2(ctx, a.src, sizeof(double) * static_cast<size_t>(n_src) * a.ld);
-    for (const HsBatch& b : P.batches) {
-      if (b.seg1 > b.seg0 && NB <= 20) {
-        using WS = WsShape<NB>;
-        const int nseg = b.seg1 - b.seg0;
-        static int per_sm = 0;
-        if (per_sm == 0) {
-          AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hs_gram_ws<NB>, (WS::GR + 1) * 32,
-                                                                 WS::smem_bytes()));
-          per_sm = std::max(per_sm, 1);
-        }
-        const int grid = std::min(nseg, per_sm * ctx->sm_count);  // persistent CTAs
-        const int tok = ctx->begin_launch("halfsweep_gram");
-        k_hs_gram_ws<NB><<<grid, (WS::GR + 1) * 32, WS::smem_bytes(), ctx->stream>>>(
-            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G);
-        ctx->end_launch(tok);
-      } else if (b.seg1 > b.seg0) {
-        const int tok = ctx->begin_launch("halfsweep_gram");
-        k_hs_gram<NB><<<b.seg1 - b.seg0, GS::W * 32, gsmem, ctx->stream>>>(
-            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
-        ctx->end_launch(tok);
-      }
-      SolveArgs s;
-      s.row0 = b.row0;
-      s.nrows = b.row1 - b.row0;
-      s.row_slot0 = P.row_slot0;
-      s.row_nslot = P.row_nslot;
-      s.G = G;
-      const int tok = ctx->begin_launch("halfsweep_solve");
-      if (kSolveCta && NB >= 9) {
-        const size_t csmem = sizeof(double) * SC::PER_WARP;
-        k_hs_solve_cta<NB><<<s.nrows, kSolveCtaWarps * 32, csmem, ctx->stream>>>(a, s);
-      } else {
-        k_hs_solve<NB><<<(s.nrows + SC::WPB - 1) / SC::WPB, SC::WPB * 32, ssmem, ctx->stream>>>(a, s);
-      }
-      ctx->end_launch(tok);
-    }
-  }
-}
-
 int hs_segment_size(int n_f) {
   if (n_f <= 32) return 8192;
   if (n_f <= 64) return 4096;
@@ -1378,7 +215,7 @@ void launch_half_sweep(DevRatings& R, int kind, int n_f, const double* src_rows,
   switch (gram_blocks(n_f)) {
 #define AB2_HS_CASE(NB) \
   case NB:              \
-    run_hs<NB>(ctx, R, kind, a, hs_segment_size(n_f)); \
+    hs::run_hs<NB>(ctx, R, kind, a, hs_segment_size(n_f)); \
     break;
     AB2_HS_CASE(1) AB2_HS_CASE(2) AB2_HS_CASE(3) AB2_HS_CASE(4) AB2_HS_CASE(5) AB2_HS_CASE(6)
     AB2_HS_CASE(7) AB2_HS_CASE(8) AB2_HS_CASE(9) AB2_HS_CASE(10) AB2_HS_CASE(11) AB2_HS_CASE(12)
