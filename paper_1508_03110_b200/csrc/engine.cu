@@ -312,12 +312,13 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
   auto P = std::make_unique<HsPlan>();
   P->S = S;
   std::vector<int> row_slot0(std::max(v.nrows, 1), 0), row_nslot(std::max(v.nrows, 1), 0);
-  std::vector<int> srow, slen, sslot;
+  std::vector<int> srow, slen, sslot, multi;
   std::vector<int64_t> sbeg;
   int r = 0;
   while (r < v.nrows) {
     HsBatch b;
     b.row0 = r;
+    b.multi0 = static_cast<int>(multi.size());
     b.seg0 = static_cast<int>(srow.size());
     int slots = 0;
     std::vector<int> order;  // segment ids of this batch
@@ -328,6 +329,7 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
       if (slots > 0 && slots + ns > max_slots) break;
       row_slot0[r] = slots;
       row_nslot[r] = ns;
+      if (ns > 1) multi.push_back(r);
       for (int s2 = 0; s2 < ns; ++s2) {
         srow.push_back(r);
         sbeg.push_back(v.h_ptr[r] + static_cast<int64_t>(s2) * S);
@@ -354,6 +356,7 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
     std::copy(s2v.begin(), s2v.end(), sslot.begin() + first);
     std::copy(b2v.begin(), b2v.end(), sbeg.begin() + first);
     b.row1 = r;
+    b.multi1 = static_cast<int>(multi.size());
     b.seg1 = static_cast<int>(srow.size());
     b.nslots = slots;
     P->max_batch_slots = std::max(P->max_batch_slots, slots);
@@ -361,7 +364,8 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
   }
   const size_t ns = std::max<size_t>(srow.size(), 1), nr = std::max<size_t>(v.nrows, 1);
   char* blk = nullptr;
-  AB2_CUDA(cudaMalloc(&blk, ns * (8 + 4 + 4 + 4) + nr * 8 + 64));
+  const size_t nm = std::max<size_t>(multi.size(), 1);
+  AB2_CUDA(cudaMalloc(&blk, ns * (8 + 4 + 4 + 4) + nr * 8 + nm * 4 + 64));
   P->block = blk;
   P->seg_beg = reinterpret_cast<int64_t*>(blk);
   P->seg_row = reinterpret_cast<int*>(blk + ns * 8);
@@ -369,6 +373,7 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
   P->seg_slot = P->seg_len + ns;
   P->row_slot0 = P->seg_slot + ns;
   P->row_nslot = P->row_slot0 + nr;
+  P->multi_rows = P->row_nslot + nr;
   auto up = [&](void* d, const void* h, size_t n) {
     if (n) AB2_CUDA(cudaMemcpy(d, h, n, cudaMemcpyHostToDevice));
   };
@@ -378,6 +383,7 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
   up(P->seg_slot, sslot.data(), sslot.size() * 4);
   up(P->row_slot0, row_slot0.data(), static_cast<size_t>(v.nrows) * 4);
   up(P->row_nslot, row_nslot.data(), static_cast<size_t>(v.nrows) * 4);
+  up(P->multi_rows, multi.data(), multi.size() * 4);
   const HsPlan& ref = *P;
   m.emplace(key, std::move(P));
   return ref;

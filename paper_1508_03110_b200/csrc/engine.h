@@ -128,9 +128,10 @@ constexpr int kTileRows = 64;  // quartic/loss tile height (rows per CTA)
 // every segment owns one slot, a row's slots are contiguous (row_slot0,
 // row_nslot, local to the batch) and segments are ordered heavy-first.
 struct HsBatch {
-  int row0, row1;  // local rows [row0, row1)
-  int seg0, seg1;  // segments of the batch
+  int row0, row1;      // local rows [row0, row1)
+  int seg0, seg1;      // segments of the batch
   int nslots;
+  int multi0, multi1;  // rows with more than one partial slot: multi_rows[multi0, multi1)
 };
 struct HsPlan {
   int S = 0;
@@ -141,6 +142,7 @@ struct HsPlan {
   int* seg_slot = nullptr;
   int* row_slot0 = nullptr;
   int* row_nslot = nullptr;
+  int* multi_rows = nullptr;
   int max_batch_slots = 0;
   void* block = nullptr;
 };

@@ -4,6 +4,9 @@
 // design notes and k_halfsweep.cu for the dispatcher and fallback.
 #include "k_halfsweep.cuh"
 
+#include <cstdlib>
+#include <utility>
+
 #ifndef AB2_HS_NB
 #error "compile with -DAB2_HS_NB=<block count>"
 #endif
@@ -1021,6 +1024,388 @@ __global__ void __launch_bounds__(kSolveCtaWarps * 32) k_hs_solve_cta(HsArgs a, 
   for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
 }
 
+// K3 (static-schedule form): one 4-warp CTA per column, right-looking blocked
+// LDL^T on the swizzled shared-memory block store, with the whole schedule
+// resolved at compile time (panel J, block coordinates and owning warp are
+// template constants, so the instruction stream is the arithmetic plus
+// immediate-offset shared loads/stores):
+//   F(J)  warp 0 factors the 8x8 diagonal block (lanes = rows, pivots by
+//         shuffle) and publishes 1/d and the 28 in-block coefficients;
+//   T(J)  one thread per row below the diagonal eliminates it against the
+//         block (TRSM form) and writes X = L~(I,J) and S = -X D^-1;
+//   U(J)  warps 1..3 apply C(I,K) += X_I S_K^T (two DMMAs per block,
+//         column-major chunks so S_K fragments are reused) while warp 0
+//         updates the next diagonal block and immediately factors it
+//         (F(J+1) overlaps the rest of U(J)).
+// Two CTA barriers per panel.  Back substitution by warp 0 as in k_hs_solve.
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  [&]<int... Is>(std::integer_sequence<int, Is...>) { (f(std::integral_constant<int, Is>{}), ...); }(
+      std::make_integer_sequence<int, N>{});
+}
+
+constexpr int kSwWarps = 4;
+
+template <int NB, int W>
+struct SwSched {
+  static constexpr int P = NB * (NB + 1) / 2;
+  // U(J) blocks (I,K), J < K <= I < NB, column-major, without (J+1,J+1)
+  static constexpr int count(int J) { return (NB - 1 - J) * (NB - J) / 2 - 1; }
+  static constexpr int order(int J, int I, int K) {
+    return (K - 1 - J) * NB - ((K - 1) * K / 2 - J * (J + 1) / 2) + (I - K) - 1;
+  }
+  static constexpr int owner(int J, int I, int K) {
+    return (I == J + 1 && K == J + 1) ? 0 : 1 + order(J, I, K) * (W - 1) / count(J);
+  }
+  static constexpr int cidx(int c) { return c * 7 - c * (c - 1) / 2; }  // first coefficient of column c
+  // shared layout (doubles)
+  static constexpr int OFF_S = P * 64;             // NB blocks: -X D^-1 of the current panel
+  static constexpr int OFF_C = OFF_S + NB * 64;    // 28 TRSM coefficients (+4)
+  static constexpr int OFF_DINV = OFF_C + 32;      // NB*8
+  static constexpr int OFF_W = OFF_DINV + NB * 8;  // NB*8 back-substitution vector
+  static constexpr int SMEM = OFF_W + NB * 8;
+};
+
+// F(J): factor the diagonal block (warp 0): lane rr holds row rr (four
+// replicas per warp), pivots by shuffle.  Publishes the factored rows, 1/d
+// and the 28 in-block coefficients L(c2, c).  Returns false on a
+// non-positive pivot (uniform across the warp).
+template <int NB, int W, int J>
+__device__ __forceinline__ bool sw_factor(double* M, int n_f, int lane) {
+  using SS = SwSched<NB, W>;
+  double* D = M + pidx(J, J) * 64;
+  double* coef = M + SS::OFF_C;
+  double* dinv = M + SS::OFF_DINV;
+  const int rr = lane & 7;
+  __syncwarp();  // the block was just updated by this warp's lanes
+  double row[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int k = 8 * J + c;
+    double inv = 0.0;
+    if (k < n_f) {
+      const double d = __shfl_sync(kFull, row[c], c);
+      if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
+        ok = false;
+        break;
+      }
+      inv = fast_rcp(d);
+      const double l = row[c] * inv;
+#pragma unroll
+      for (int c2 = c + 1; c2 < 8; ++c2) {
+        const double av = __shfl_sync(kFull, row[c], c2);  // A(c2, c)
+        if (rr > c && c2 <= rr) row[c2] = fma(-l, av, row[c2]);
+      }
+    }
+    if (lane == 0) dinv[k] = inv;
+    if (c < 7 && lane < 8 && rr > c) coef[SS::cidx(c) + rr - c - 1] = row[c] * inv;  // L(rr, c)
+  }
+  if (ok && lane < 8)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c <= rr) D[swz(rr, c)] = row[c];
+  return ok;
+}
+
+// T(J): eliminate every row of the blocks below the diagonal (one per thread).
+
+template <int NB, int W, int J>
+__device__ __forceinline__ void sw_trsm_row(double* M, int row) {
+  using SS = SwSched<NB, W>;
+  const int I = J + 1 + (row >> 3), rr = row & 7;
+  const bool sw = (rr >> 1) & 1;  // swizzle: columns 0-3 and 4-7 swap halves
+  double2* xr = reinterpret_cast<double2*>(M + (I * (I + 1) / 2 + J) * 64 + 8 * rr);
+  double2* sr = reinterpret_cast<double2*>(M + SS::OFF_S + I * 64 + 8 * rr);
+  const double2* cf = reinterpret_cast<const double2*>(M + SS::OFF_C);
+  const double2* dv = reinterpret_cast<const double2*>(M + SS::OFF_DINV + 8 * J);
+  double x[8];
+  {
+    const double2 v0 = xr[0], v1 = xr[1], v2 = xr[2], v3 = xr[3];
+    x[0] = sw ? v2.x : v0.x; x[1] = sw ? v2.y : v0.y; x[2] = sw ? v3.x : v1.x; x[3] = sw ? v3.y : v1.y;
+    x[4] = sw ? v0.x : v2.x; x[5] = sw ? v0.y : v2.y; x[6] = sw ? v1.x : v3.x; x[7] = sw ? v1.y : v3.y;
+  }
+  double cc[28];
+#pragma unroll
+  for (int u = 0; u < 14; ++u) {
+    const double2 v = cf[u];
+    cc[2 * u] = v.x;
+    cc[2 * u + 1] = v.y;
+  }
+  {
+    int u = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], cc[u++], x[c2]);
+  }
+  double iv[8];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const double2 v = dv[h];
+    iv[2 * h] = v.x;
+    iv[2 * h + 1] = v.y;
+  }
+  double s[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s[c] = -x[c] * iv[c];
+  const int a = sw ? 2 : 0, b = sw ? 0 : 2;
+  xr[a] = make_double2(x[0], x[1]);
+  xr[a + 1] = make_double2(x[2], x[3]);
+  xr[b] = make_double2(x[4], x[5]);
+  xr[b + 1] = make_double2(x[6], x[7]);
+  sr[a] = make_double2(s[0], s[1]);
+  sr[a + 1] = make_double2(s[2], s[3]);
+  sr[b] = make_double2(s[4], s[5]);
+  sr[b + 1] = make_double2(s[6], s[7]);
+}
+
+template <int NB, int W, int J>
+__device__ __forceinline__ void sw_trsm(double* M, int tid) {
+  constexpr int ROWS = 8 * (NB - 1 - J);
+  for (int row = tid; row < ROWS; row += W * 32) sw_trsm_row<NB, W, J>(M, row);
+}
+
+// Compile-time list of the U(J) blocks warp w owns (column-major order).
+template <int NB, int W>
+struct SwList {
+  int n;
+  int I[NB * (NB + 1) / 2];
+  int K[NB * (NB + 1) / 2];
+  static constexpr SwList make(int J, int w) {
+    SwList l{};
+    for (int k = J + 1; k < NB; ++k)
+      for (int i = k; i < NB; ++i)
+        if (SwSched<NB, W>::owner(J, i, k) == w) {
+          l.I[l.n] = i;
+          l.K[l.n] = k;
+          ++l.n;
+        }
+    return l;
+  }
+};
+
+template <int NB, int W, int J, int w>
+struct SwL {
+  static constexpr SwList<NB, W> v = SwList<NB, W>::make(J, w);
+};
+
+// U(J) for warp w: C(I,K) += X_I S_K^T (S holds -X D^-1), G blocks at a time
+// with every load of a group issued before its DMMAs and stores (the
+// blocks are independent; the compiler cannot prove it through the lane
+// offsets, so the batching is explicit).
+template <int NB, int W, int J, int w>
+__device__ __forceinline__ void sw_update(double* M, int oc, int oa0, int oa1) {
+  using SS = SwSched<NB, W>;
+  using L = SwL<NB, W, J, w>;
+  constexpr int G = 4;
+  static_for<(L::v.n + G - 1) / G>([&](auto gc) {
+    constexpr int g0 = decltype(gc)::value * G;
+    double2 c[G];
+    double xa[G][2], sb[G][2];
+    static_for<G>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if constexpr (g0 + i < L::v.n) {
+        constexpr int I = L::v.I[g0 + i], K = L::v.K[g0 + i];
+        c[i] = *reinterpret_cast<const double2*>(M + (I * (I + 1) / 2 + K) * 64 + oc);
+        xa[i][0] = M[(I * (I + 1) / 2 + J) * 64 + oa0];
+        xa[i][1] = M[(I * (I + 1) / 2 + J) * 64 + oa1];
+        sb[i][0] = M[SS::OFF_S + K * 64 + oa0];
+        sb[i][1] = M[SS::OFF_S + K * 64 + oa1];
+      }
+    });
+    static_for<G>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if constexpr (g0 + i < L::v.n) dmma884(c[i].x, c[i].y, xa[i][0], sb[i][0]);
+    });
+    static_for<G>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if constexpr (g0 + i < L::v.n) dmma884(c[i].x, c[i].y, xa[i][1], sb[i][1]);
+    });
+    static_for<G>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if constexpr (g0 + i < L::v.n) {
+        constexpr int I = L::v.I[g0 + i], K = L::v.K[g0 + i];
+        *reinterpret_cast<double2*>(M + (I * (I + 1) / 2 + K) * 64 + oc) = c[i];
+      }
+    });
+  });
+}
+
+#ifdef AB2_SW_PROBE
+// development probe: per-phase clocks of the first 64 columns (warp 0, lane 0)
+__device__ unsigned long long g_sw_probe[64][64];
+#define SW_PROBE(slot) \
+  do { if ((blockIdx.x & 1023) == 0 && blockIdx.x < 65536 && (threadIdx.x & 127) == 0) g_sw_probe[blockIdx.x >> 10][slot] = clock64(); } while (0)
+#define SW_PROBE_W(slot) \
+  do { if ((blockIdx.x & 1023) == 0 && blockIdx.x < 65536 && (threadIdx.x & 31) == 0) g_sw_probe[blockIdx.x >> 10][slot] = clock64(); } while (0)
+#else
+#define SW_PROBE(slot) do {} while (0)
+#define SW_PROBE_W(slot) do {} while (0)
+#endif
+
+// The factorization proper for warp w; false if a pivot was non-positive.
+template <int NB, int W, int w>
+__device__ __forceinline__ bool sw_run(double* M, int n_f, int tid, int lane, volatile int* fail) {
+  using SS = SwSched<NB, W>;
+  const int KP = (n_f + 7) >> 3;
+  const int r = lane >> 2, q = lane & 3;
+  const int oc = swz(r, 2 * q), oa0 = swz(r, q), oa1 = swz(r, 4 + q);
+  if constexpr (w == 0)
+    if (!sw_factor<NB, W, 0>(M, n_f, lane) && lane == 0) *fail = 1;
+  __syncthreads();
+  if (*fail) return false;
+  bool ok = true;
+  static_for<NB>([&](auto Jc) {
+    constexpr int J = decltype(Jc)::value;
+    if (!ok || J >= KP) return;
+    SW_PROBE(2 + 4 * J);
+    sw_trsm<NB, W, J>(M, tid);
+    SW_PROBE(3 + 4 * J);
+    __syncthreads();
+    if constexpr (J + 1 < NB) {
+      // (blocks of column NB-1 are updated even when it is not a pivot
+      // column: harmless, they are never read again)
+      SW_PROBE(4 + 4 * J);
+      sw_update<NB, W, J, w>(M, oc, oa0, oa1);
+      if constexpr (w == 0) {
+        SW_PROBE_W(5 + 4 * J);
+        if (J + 1 < KP && !sw_factor<NB, W, J + 1>(M, n_f, lane) && lane == 0) *fail = 1;
+      }
+    }
+    __syncthreads();
+    if (*fail) ok = false;
+  });
+  return ok;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kSwWarps * 32) k_hs_solve_sw(HsArgs a, SolveArgs s) {
+  using C = SolveCfg<NB>;
+  using SS = SwSched<NB, kSwWarps>;
+  constexpr int NT = kSwWarps * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  SW_PROBE(0);
+  const int lr = s.row0 + blockIdx.x;
+  const int n_f = a.n_f, ld = a.ld;
+  double* M = g_smem;
+  double* dinv = M + SS::OFF_DINV;
+  double* w = M + SS::OFF_W;
+  __shared__ int fail;
+  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
+  if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
+    for (int k = tid; k < ld; k += NT) out[k] = 0.0;
+    return;
+  }
+  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
+  if (!(shift > 0.0)) {
+    if (tid == 0) {
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  const int r = lane >> 2, q = lane & 3;
+  {
+    // heavy rows were folded into their first slot by k_hs_slot_reduce
+    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
+    for (int p = warp; p < C::P; p += kSwWarps) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
+    cp_async_commit();
+    cp_async_wait<0>();
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int k = tid; k < n_f; k += NT) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;  // als.cpp:58-59
+    __syncthreads();
+  }
+  SW_PROBE(1);
+  bool ok;
+  switch (warp) {
+    case 0: ok = sw_run<NB, kSwWarps, 0>(M, n_f, tid, lane, &fail); break;
+    case 1: ok = sw_run<NB, kSwWarps, 1>(M, n_f, tid, lane, &fail); break;
+    case 2: ok = sw_run<NB, kSwWarps, 2>(M, n_f, tid, lane, &fail); break;
+    default: ok = sw_run<NB, kSwWarps, 3>(M, n_f, tid, lane, &fail); break;
+  }
+  if (!ok) {
+    if (tid == 0) {
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+    return;
+  }
+  SW_PROBE(60);
+  // Back substitution, all warps: u_k = (w_k - sum_{i>k} A~(i,k) u_i) / d_k,
+  // one 8-row block at a time: every thread solves the block's 8 unknowns
+  // from registers (same arithmetic in every thread), then thread i < 8K
+  // folds them into w_i.
+  const int KP = (n_f + 7) >> 3;
+  {
+    const int IR = ld >> 3, rl = ld & 7;
+    for (int k = tid; k < n_f; k += NT) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rl, k & 7)];
+  }
+  __syncthreads();
+  for (int K = KP - 1; K >= 0; --K) {
+    const double* D = M + pidx(K, K) * 64;
+    double u[8];
+#pragma unroll
+    for (int c = 7; c >= 0; --c) {
+      double v = 0.0;
+      if (8 * K + c < n_f) {
+        v = w[8 * K + c];
+#pragma unroll
+        for (int i = 7; i > c; --i) v = fma(-D[swz(i, c)], u[i], v);  // u[c+1] (latest) last
+        v *= dinv[8 * K + c];
+      }
+      u[c] = v;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (tid == c && 8 * K + c < n_f) out[8 * K + c] = u[c];
+    for (int i = tid; i < 8 * K; i += NT) {
+      const double* blk = M + pidx(K, i >> 3) * 64;
+      double acc = w[i];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc = fma(-blk[swz(c, i & 7)], u[c], acc);
+      w[i] = acc;
+    }
+    __syncthreads();
+  }
+  for (int k = n_f + tid; k < ld; k += NT) out[k] = 0.0;
+  SW_PROBE(61);
+}
+
+// Heavy rows: fold a row's partial Gram slots into its first slot, in slot
+// order (deterministic; every load of a thread is independent, so all slots
+// of a row are in flight at once).  One thread per double2 of one row.
+__global__ void __launch_bounds__(256) k_hs_slot_reduce(const int* __restrict__ rows, int n_rows,
+                                                        const int* __restrict__ row_slot0,
+                                                        const int* __restrict__ row_nslot, double* G,
+                                                        int slot_d2) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(n_rows) * slot_d2) return;
+  const int m = static_cast<int>(e / slot_d2), i = static_cast<int>(e % slot_d2);
+  const int row = rows[m];
+  double2* base = reinterpret_cast<double2*>(G) + static_cast<int64_t>(row_slot0[row]) * slot_d2 + i;
+  const int ns = row_nslot[row];
+  double2 v = base[0];
+  int t = 1;
+  for (; t + 4 <= ns; t += 4) {
+    const double2 a = base[static_cast<int64_t>(t) * slot_d2], b = base[static_cast<int64_t>(t + 1) * slot_d2];
+    const double2 c = base[static_cast<int64_t>(t + 2) * slot_d2], d = base[static_cast<int64_t>(t + 3) * slot_d2];
+    v.x += a.x; v.y += a.y;
+    v.x += b.x; v.y += b.y;
+    v.x += c.x; v.y += c.y;
+    v.x += d.x; v.y += d.y;
+  }
+  for (; t < ns; ++t) {
+    const double2 a = base[static_cast<int64_t>(t) * slot_d2];
+    v.x += a.x; v.y += a.y;
+  }
+  base[0] = v;
+}
+
 template <int NB>
 struct Mode {
   static constexpr int GW = NB <= 4 ? 1 : (NB <= 16 ? 4 : (NB <= 20 ? 8 : 16));
@@ -1033,6 +1418,8 @@ template <int NB>
 constexpr bool kGramWs = NB <= 20;                // warp-specialised persistent Gram
 template <int NB>
 constexpr bool kSolveCtaFor = kSolveCta && NB >= 9;
+template <int NB>
+constexpr bool kSolveSwFor = true;                // static-schedule CTA solve (k_hs_solve_sw)
 
 template <int NB>
 void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
@@ -1086,7 +1473,10 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
         AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       else
         AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      if constexpr (kSolveCtaFor<NB>)  // exact size: the kernel also has static shared memory
+      if constexpr (kSolveSwFor<NB>) {
+        AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_sw<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sizeof(double) * SwSched<NB, kSwWarps>::SMEM)));
+      } else if constexpr (kSolveCtaFor<NB>)  // exact size: the kernel also has static shared memory
         AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_cta<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sizeof(double) * SC::PER_WARP)));
       else
@@ -1127,8 +1517,20 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       s.row_slot0 = P.row_slot0;
       s.row_nslot = P.row_nslot;
       s.G = G;
+      if constexpr (kSolveSwFor<NB>) {
+        if (b.multi1 > b.multi0) {  // the solve reads one (folded) slot per row
+          const int slot_d2 = C::P * 32;
+          const int64_t n = static_cast<int64_t>(b.multi1 - b.multi0) * slot_d2;
+          const int tok = ctx->begin_launch("halfsweep_slot_reduce");
+          k_hs_slot_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
+              P.multi_rows + b.multi0, b.multi1 - b.multi0, P.row_slot0, P.row_nslot, G, slot_d2);
+          ctx->end_launch(tok);
+        }
+      }
       const int tok = ctx->begin_launch("halfsweep_solve");
-      if constexpr (kSolveCtaFor<NB>) {
+      if constexpr (kSolveSwFor<NB>) {
+        k_hs_solve_sw<NB><<<s.nrows, kSwWarps * 32, sizeof(double) * SwSched<NB, kSwWarps>::SMEM, ctx->stream>>>(a, s);
+      } else if constexpr (kSolveCtaFor<NB>) {
         const size_t csmem = sizeof(double) * SC::PER_WARP;
         k_hs_solve_cta<NB><<<s.nrows, kSolveCtaWarps * 32, csmem, ctx->stream>>>(a, s);
       } else {
@@ -1148,3 +1550,11 @@ void run_hs<AB2_HS_NB>(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
 
 }  // namespace hs
 }  // namespace ab2
+
+#ifdef AB2_SW_PROBE
+#define AB2_CAT2(a, b) a##b
+#define AB2_CAT(a, b) AB2_CAT2(a, b)
+extern "C" int AB2_CAT(alsncg_debug_sw_probe_, AB2_HS_NB)(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, ab2::hs::g_sw_probe, sizeof(ab2::hs::g_sw_probe)));
+}
+#endif
