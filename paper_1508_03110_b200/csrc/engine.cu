@@ -16,6 +16,9 @@ Ctx::Ctx(int dev) : device(dev) {
   AB2_CUDA(cudaSetDevice(dev));
   AB2_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
   AB2_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  AB2_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  AB2_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  AB2_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   AB2_CUDA(cudaMalloc(&d_red, sizeof(double) * 2 * 8 * 4 * 148));
   AB2_CUDA(cudaMalloc(&d_counters, sizeof(unsigned) * 64));
   AB2_CUDA(cudaMemset(d_counters, 0, sizeof(unsigned) * 64));
@@ -39,6 +42,12 @@ Ctx::~Ctx() {
   cudaFree(d_scalars);
   cudaFreeHost(h_scalars);
   if (comm) nccl().CommDestroy(comm);
+  if (side) {
+    cudaStreamSynchronize(side);
+    cudaStreamDestroy(side);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   if (stream) cudaStreamDestroy(stream);
 }
 

@@ -61,6 +61,10 @@ struct Ctx {
   int rank = 0;
   int world = 1;
   cudaStream_t stream = nullptr;
+  // Side stream for work that is independent of the main chain (the NCG
+  // gradient at x_{k+1} runs beside the two half-sweeps P(x_{k+1})).
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ncclComm_t comm = nullptr;
   bool profiling = false;
   int64_t launches = 0;

@@ -21,6 +21,9 @@ namespace ab2 {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+// Gradient CTAs are small so they fit beside the half-sweep kernels, which
+// they run concurrently with (side stream, Solver::ncg_iteration).
+constexpr int kGradWarps = 2;
 
 template <int TPR>
 __device__ __forceinline__ double group_sum(double v) {
@@ -67,9 +70,9 @@ struct GradArgs {
 };
 
 template <int TPR, int V2>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_gradient(GradArgs a) {
+__global__ void __launch_bounds__(kGradWarps * 32) k_gradient(GradArgs a) {
   const int lane = threadIdx.x & 31;
-  const int seg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int seg = blockIdx.x * kGradWarps + (threadIdx.x >> 5);
   if (seg >= a.n_seg) return;
   constexpr int R = 32 / TPR;
   const int sg = lane / TPR, sl = lane % TPR;
@@ -275,6 +278,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_quartic(QuartArgs a) {
         }
       }
     }
+
   } else {
     // item regularisation rows (linesearch.cpp:90-103; ncg.cpp:62-66)
     const int hi = min(lo + kTileRows, a.nirows);
@@ -396,9 +400,9 @@ void launch_gradient(DevRatings& R, int n_f, const double* x, double lambda, dou
     a.n_seg = P.n_seg;
     a.g = g;
     a.partial = partial;
-    const int blocks = (P.n_seg + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int blocks = (P.n_seg + kGradWarps - 1) / kGradWarps;
     const int tok = ctx->begin_launch(kind == 0 ? "gradient_users" : "gradient_items");
-#define AB2_LAUNCH_GRAD(T, V) k_gradient<T, V><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(a)
+#define AB2_LAUNCH_GRAD(T, V) k_gradient<T, V><<<blocks, kGradWarps * 32, 0, ctx->stream>>>(a)
     AB2_GEOM_DISPATCH(geo, AB2_LAUNCH_GRAD);
 #undef AB2_LAUNCH_GRAD
     ctx->end_launch(tok);

@@ -248,9 +248,24 @@ void Solver::ncg_iteration() {
   } else {
     launch_axpby(ctx_, N_, 1.0, x_, alpha, p_, xn_);
   }
-  gradient(xn_, gn_);  // ncg.cpp:253
+  // ncg.cpp:253-255: the gradient at x_{k+1} and P(x_{k+1}) only read
+  // x_{k+1}; on one GPU the gradient runs on the side stream beside the two
+  // half-sweeps (latency-bound solves leave the SMs room for its gathers).
+  // With NCCL exchanges in both, the multi-GPU path keeps them in order.
+  if (ctx_->world == 1) {
+    AB2_CUDA(cudaEventRecord(ctx_->ev_fork, ctx_->stream));
+    AB2_CUDA(cudaStreamWaitEvent(ctx_->side, ctx_->ev_fork, 0));
+    std::swap(ctx_->stream, ctx_->side);
+    gradient(xn_, gn_);
+    std::swap(ctx_->stream, ctx_->side);
+    AB2_CUDA(cudaEventRecord(ctx_->ev_join, ctx_->side));
+    apply_als(xn_, pxn_);
+    AB2_CUDA(cudaStreamWaitEvent(ctx_->stream, ctx_->ev_join, 0));
+  } else {
+    gradient(xn_, gn_);
+    apply_als(xn_, pxn_);
+  }
   step_columns_ += gradient_columns_;
-  apply_als(xn_, pxn_);  // ncg.cpp:255
   step_columns_ += sweep_columns_;
   // gbar_next, beta parts, ||g_next||^2 and g_next.(-gbar_next) in one pass
   launch_vec(ctx_, kGbarFused, N_, xn_, pxn_, gn_, g_, 0.0, gbn_, kSlotGbar);
