@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -65,6 +66,11 @@ struct Ctx {
   // gradient at x_{k+1} runs beside the two half-sweeps P(x_{k+1})).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // Work to enqueue on `side` once the next half-sweep has launched its first
+  // Gram kernel (it then overlaps that batch's latency-bound solve, not the
+  // DMMA-bound Gram); the main stream joins before the following Gram.
+  std::function<void()> side_work;
+  bool side_join = false;
   ncclComm_t comm = nullptr;
   bool profiling = false;
   int64_t launches = 0;

@@ -1489,6 +1489,10 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     const int n_src = kind == 0 ? R.n_m : R.n_u;
     L2Window l2(ctx, a.src, sizeof(double) * static_cast<size_t>(n_src) * a.ld);
     for (const HsBatch& b : P.batches) {
+      if (ctx->side_join) {  // side work runs beside the previous batch's solve only
+        AB2_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+        ctx->side_join = false;
+      }
       if constexpr (kGramWs<NB>) {
         if (b.seg1 > b.seg0) {
           using WS = WsShape<NB>;
@@ -1510,6 +1514,13 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
         k_hs_gram<NB><<<b.seg1 - b.seg0, GS::W * 32, gsmem, ctx->stream>>>(
             a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
         ctx->end_launch(tok);
+      }
+      if (ctx->side_work) {  // independent side work overlaps this batch's solve
+        AB2_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+        auto w = std::move(ctx->side_work);
+        ctx->side_work = nullptr;
+        w();
+        ctx->side_join = true;
       }
       SolveArgs s;
       s.row0 = b.row0;

@@ -253,14 +253,27 @@ void Solver::ncg_iteration() {
   // half-sweeps (latency-bound solves leave the SMs room for its gathers).
   // With NCCL exchanges in both, the multi-GPU path keeps them in order.
   if (ctx_->world == 1) {
-    AB2_CUDA(cudaEventRecord(ctx_->ev_fork, ctx_->stream));
-    AB2_CUDA(cudaStreamWaitEvent(ctx_->side, ctx_->ev_fork, 0));
-    std::swap(ctx_->stream, ctx_->side);
-    gradient(xn_, gn_);
-    std::swap(ctx_->stream, ctx_->side);
-    AB2_CUDA(cudaEventRecord(ctx_->ev_join, ctx_->side));
+    // enqueued by the first half-sweep batch after its Gram launch (ev_fork
+    // recorded there), joined before the next Gram (k_hs_inst.cu run_hs)
+    ctx_->side_work = [this]() {
+      AB2_CUDA(cudaStreamWaitEvent(ctx_->side, ctx_->ev_fork, 0));
+      std::swap(ctx_->stream, ctx_->side);
+      gradient(xn_, gn_);
+      std::swap(ctx_->stream, ctx_->side);
+      AB2_CUDA(cudaEventRecord(ctx_->ev_join, ctx_->side));
+    };
     apply_als(xn_, pxn_);
-    AB2_CUDA(cudaStreamWaitEvent(ctx_->stream, ctx_->ev_join, 0));
+    if (ctx_->side_work) {  // no split half-sweep consumed it (small ranks): run it in order
+      AB2_CUDA(cudaEventRecord(ctx_->ev_fork, ctx_->stream));
+      auto w = std::move(ctx_->side_work);
+      ctx_->side_work = nullptr;
+      w();
+      ctx_->side_join = true;
+    }
+    if (ctx_->side_join) {
+      AB2_CUDA(cudaStreamWaitEvent(ctx_->stream, ctx_->ev_join, 0));
+      ctx_->side_join = false;
+    }
   } else {
     gradient(xn_, gn_);
     apply_als(xn_, pxn_);

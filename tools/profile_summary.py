@@ -21,7 +21,8 @@ def launches(src, dst):
             continue
         name = r[iK].split("(")[0].replace("void ", "").replace("ab2::<unnamed>::", "")
         v = float(r[iV].replace(",", ""))
-        v = v / 1e3 if r[iU] == "nsecond" else (v * 1e3 if r[iU] == "msecond" else v)
+        u = r[iU]
+        v = v / 1e3 if u in ("ns", "nsecond") else (v * 1e3 if u in ("ms", "msecond") else v)  # -> us
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
@@ -44,7 +45,8 @@ def kernel(rep, dst):
             "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
-            "smsp__inst_executed.avg.per_cycle_active"]
+            "smsp__inst_executed.avg.per_cycle_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__throughput.avg.pct_of_peak_sustained_active"]
     cols = [h for h in want if h in hdr]
     out = [f"# ncu --set full summary ({rep})", "", "| " + " | ".join(cols) + " |",
            "|" + "---|" * len(cols), "| " + " | ".join(units[hdr.index(c)] for c in cols) + " |"]
