@@ -159,6 +159,11 @@ int alsncg_ratings_download(alsncg_ratings* r, int64_t* uptr, int* uidx, double*
                             int64_t* iptr, int* iidx, double* ival);
 /* Local shard: users [u0,u1) and items [m0,m1) owned by this rank. */
 int alsncg_ratings_shard(alsncg_ratings* r, int* u0, int* u1, int* m0, int* m1);
+/* Host only (no device): the shard bounds every rank computes for a CSR/CSC
+ * pointer array -- world+1 row bounds, nnz-balanced, interior bounds rounded
+ * to multiples of `align` rows (the quartic/loss tile size, 64).  Replaces the
+ * reference's block routing (parallel.cpp:57-142) for the row-sharded layout. */
+int alsncg_partition_rows(int n_rows, const int64_t* ptr, int world, int align, int* bounds);
 int alsncg_ratings_free(alsncg_ratings* r);
 
 /* ---------------- hot-path kernels, HOST buffers (reference-facing) -------- */

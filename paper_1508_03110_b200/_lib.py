@@ -68,6 +68,7 @@ SIGNATURES = {
     "alsncg_ratings_upload": (i32, [vp, i32, i32, i64, vp, vp, vp, vp, vp, vp, C.POINTER(vp)]),
     "alsncg_ratings_download": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "alsncg_ratings_shard": (i32, [vp, ip, ip, ip, ip]),
+    "alsncg_partition_rows": (i32, [i32, vp, i32, i32, vp]),
     "alsncg_ratings_free": (i32, [vp]),
     "alsncg_loss": (i32, [vp, i32, vp, f64, dp]),
     "alsncg_gradient": (i32, [vp, i32, vp, f64, vp]),

@@ -293,6 +293,15 @@ int alsncg_ratings_shard(alsncg_ratings* r, int* u0, int* u1, int* m0, int* m1) 
   });
 }
 
+int alsncg_partition_rows(int n_rows, const int64_t* ptr, int world, int align, int* bounds) {
+  return guarded([&] {
+    if (n_rows < 0 || world < 1 || align < 1 || ptr == nullptr || bounds == nullptr)
+      throw ab2::Error(ALSNCG_EINVAL, "alsncg_partition_rows: bad arguments");
+    const std::vector<int> b = ab2::partition_rows(n_rows, ptr, world, align);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
 int alsncg_ratings_free(alsncg_ratings* r) {
   return guarded([&] {
     if (r) AB2_CUDA(cudaSetDevice(r->impl->ctx->device));
