@@ -3,6 +3,8 @@
 // line; every vector lives in HBM, each iteration moves ~10 doubles over PCIe.
 #include "solver.h"
 
+#include <cstdlib>
+
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -252,7 +254,11 @@ void Solver::ncg_iteration() {
   // x_{k+1}; on one GPU the gradient runs on the side stream beside the two
   // half-sweeps (latency-bound solves leave the SMs room for its gathers).
   // With NCCL exchanges in both, the multi-GPU path keeps them in order.
-  if (ctx_->world == 1) {
+  // Opt-in (ALSNCG_OVERLAP=1): measured neutral-to-slightly-negative on one
+  // B200 at n_f = 25..100 (the gradient's FP64 gathers and the latency-bound
+  // solve contend for the same sub-partitions), so the default keeps order.
+  static const bool overlap = std::getenv("ALSNCG_OVERLAP") != nullptr;
+  if (ctx_->world == 1 && overlap) {
     // enqueued by the first half-sweep batch after its Gram launch (ev_fork
     // recorded there), joined before the next Gram (k_hs_inst.cu run_hs)
     ctx_->side_work = [this]() {
