@@ -231,6 +231,8 @@ void launch_axpby(Ctx* ctx, int64_t n, double a, const double* x, double b, cons
 void launch_routing_count(DevRatings& R, int n_blocks, unsigned long long* d_out2);
 // Packed <-> padded row layout conversions.
 void launch_pad_rows(Ctx* ctx, int64_t rows, int n_f, const double* packed, double* padded);
+// x0 = flatten(random_init(seed)) straight into the padded flat vector x.
+void launch_random_init(Ctx* ctx, int n_f, int n_u, int n_m, uint64_t seed, double* x);
 void launch_unpad_rows(Ctx* ctx, int64_t rows, int n_f, const double* padded, double* packed);
 
 // Multi-GPU: replicate row ranges [b[r], b[r+1]) of a row-major buffer from

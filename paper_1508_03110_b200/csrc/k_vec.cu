@@ -9,6 +9,8 @@
 // per element (K8).
 #include "common.cuh"
 
+#include <cmath>
+
 namespace ab2 {
 
 namespace {
@@ -254,6 +256,82 @@ void launch_routing_count(DevRatings& R, int n_blocks, unsigned long long* d_out
     k_routing_count<<<blocks, 256, smem, ctx->stream>>>(v.nrows, v.ptr, v.idx, n_blocks, d_out2 + kind);
     ctx->end_launch(t);
   }
+}
+
+// ------------------------------------------------------------ random_init --
+// x0 = flatten(random_init(seed)) (factors.cpp:24-32) generated on the device:
+// the mt19937_64 stream of std::mt19937_64(seed) (state seeded on the host),
+// items first then users, u = (draw >> 11) * 2^-53 * (1/sqrt(n_f)) -- the
+// same operations as the host Rng::uniform, so x0 is bitwise the reference's.
+// One CTA walks the sequential twist chain (three barriers per 312-draw
+// block); the draws land straight in the padded flat vector.
+namespace {
+constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull, kMtUpper = 0xFFFFFFFF80000000ull,
+                   kMtLower = 0x000000007FFFFFFFull;
+
+__device__ __forceinline__ uint64_t mt_twist(uint64_t cur, uint64_t next, uint64_t far) {
+  const uint64_t y = (cur & kMtUpper) | (next & kMtLower);
+  return far ^ (y >> 1) ^ ((y & 1ull) ? kMtA : 0ull);
+}
+
+__global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restrict__ state0,
+                                                          int64_t n_item_draws, int64_t n_draws,
+                                                          int n_f, int ld, int n_u, double scale,
+                                                          double* __restrict__ x) {
+  __shared__ uint64_t mt[312];
+  const int tid = threadIdx.x;
+  if (tid < 312) mt[tid] = state0[tid];
+  __syncthreads();
+  for (int64_t base = 0; base < n_draws; base += 312) {
+    uint64_t v = 0;
+    if (tid < 156) v = mt_twist(mt[tid], mt[tid + 1], mt[tid + 156]);
+    __syncthreads();
+    if (tid < 156) mt[tid] = v;
+    __syncthreads();
+    if (tid >= 156 && tid < 311) v = mt_twist(mt[tid], mt[tid + 1], mt[tid - 156]);
+    if (tid == 311) v = mt_twist(mt[311], mt[0], mt[155]);
+    __syncthreads();
+    if (tid >= 156 && tid < 312) mt[tid] = v;
+    __syncthreads();
+    const int64_t k = base + tid;
+    if (tid < 312 && k < n_draws) {
+      uint64_t z = mt[tid];
+      z ^= (z >> 29) & 0x5555555555555555ull;
+      z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+      z ^= (z << 37) & 0xFFF7EEE000000000ull;
+      z ^= z >> 43;
+      const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+      const double val = __dmul_rn(u, scale);
+      int64_t row, col;
+      if (k < n_item_draws) {
+        row = n_u + k / n_f;
+        col = k % n_f;
+      } else {
+        row = (k - n_item_draws) / n_f;
+        col = (k - n_item_draws) % n_f;
+      }
+      x[row * ld + col] = val;
+    }
+  }
+}
+}  // namespace
+
+void launch_random_init(Ctx* ctx, int n_f, int n_u, int n_m, uint64_t seed, double* x) {
+  // std::mt19937_64 seeding (linear recurrence, 312 words) on the host
+  uint64_t st[312];
+  st[0] = seed;
+  for (int i = 1; i < 312; ++i) st[i] = 6364136223846793005ull * (st[i - 1] ^ (st[i - 1] >> 62)) + i;
+  uint64_t* d = static_cast<uint64_t*>(ctx->scratch(7, sizeof st));
+  AB2_CUDA(cudaMemcpyAsync(d, st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+  const int ld = row_stride(n_f);
+  AB2_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (static_cast<size_t>(n_u) + n_m) * ld, ctx->stream));
+  const int64_t nm = static_cast<int64_t>(n_f) * n_m, nu = static_cast<int64_t>(n_f) * n_u;
+  const int t = ctx->begin_launch("random_init");
+  k_mt_random_init<<<1, 320, 0, ctx->stream>>>(d, nm, nm + nu, n_f, ld, n_u,
+                                               1.0 / std::sqrt(static_cast<double>(n_f)), x);
+  ctx->end_launch(t);
+  // the host staging array must outlive the async copy
+  AB2_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 }  // namespace ab2

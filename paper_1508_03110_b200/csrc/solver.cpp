@@ -3,6 +3,7 @@
 // line; every vector lives in HBM, each iteration moves ~10 doubles over PCIe.
 #include "solver.h"
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <cmath>
@@ -48,6 +49,14 @@ int resolved_blocks(const alsncg_config& c) {  // config.hpp:48
 Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapshot_fn snap,
                void* user)
     : R_(R), ctx_(R->ctx), cfg_(cfg), ncg_(ncg), snap_(snap), user_(user) {
+  static const bool tsetup = std::getenv("ALSNCG_SETUP_TIMING") != nullptr;
+  Watch tw;
+  tw.start();
+  auto mark = [&](const char* what) {
+    if (!tsetup) return;
+    ctx_->sync();
+    std::fprintf(stderr, "[setup] %-22s %8.2f ms\n", what, tw.seconds() * 1e3);
+  };
   validate(cfg_);
   AB2_CUDA(cudaSetDevice(ctx_->device));
   n_f_ = cfg_.n_f;
@@ -60,6 +69,7 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
   sweep_columns_ = tot.first + tot.second;  // ncg.cpp:143-151
   gradient_columns_ = sweep_columns_;
   quartic_columns_ = 2 * tot.second;
+  mark("routing");
   const int nbuf = ncg_ ? 10 : 2;
   AB2_CUDA(cudaMalloc(&buf_, sizeof(double) * std::max<int64_t>(N_, 1) * nbuf));
   double* b = buf_;
@@ -83,23 +93,20 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
     gbar_ = p_ = px_ = xn_ = gn_ = gbn_ = pn_ = pxn_ = nullptr;
   }
   AB2_CUDA(cudaMemsetAsync(ctx_->d_counters + kCounterFallback, 0, sizeof(unsigned), ctx_->stream));
+  mark("malloc");
 
-  // x0 = flatten(random_init(seed)) (ncg.cpp:154-155), uploaded in padded rows.
-  {
-    std::vector<double> host(static_cast<size_t>(Nlog_));
-    random_init(n_f_, R_->n_u, R_->n_m, cfg_.seed, host.data(),
-                host.data() + static_cast<size_t>(n_f_) * R_->n_u);
-    double* d_packed = static_cast<double*>(ctx_->scratch(6, sizeof(double) * std::max<int64_t>(Nlog_, 1)));
-    AB2_CUDA(cudaMemcpyAsync(d_packed, host.data(), sizeof(double) * Nlog_, cudaMemcpyHostToDevice,
-                             ctx_->stream));
-    launch_pad_rows(ctx_, rows_, n_f_, d_packed, x_);
-  }
+  // x0 = flatten(random_init(seed)) (ncg.cpp:154-155), generated on the
+  // device in padded rows (bitwise the host stream, k_vec.cu).
+  launch_random_init(ctx_, n_f_, R_->n_u, R_->n_m, cfg_.seed, x_);
+  mark("random_init+upload");
   // ncg.cpp:178-181 / als.cpp:150-154
   gradient(x_, g_);
+  mark("gradient(x0)");
   launch_vec(ctx_, kDot, N_, g_, g_, nullptr, nullptr, 0.0, nullptr, kSlotDot);
   ctx_->fetch_scalars(kSlotDot + 1);
   grad_norm_ = std::sqrt(ctx_->h_scalars[kSlotDot]) / static_cast<double>(Nlog_);
   append({0, loss(x_), grad_norm_, 0.0, 0, 0, 0});
+  mark("loss(x0)");
   if (snap_ && cfg_.snapshot_every > 0) snapshot(0);
   converged_ = cfg_.tol > 0.0 && grad_norm_ < cfg_.tol;
   if (!ncg_) {
@@ -119,6 +126,7 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
     restart_pending_ = false;
     step_columns_ = sweep_columns_ + gradient_columns_;
     started_ = true;
+    mark("P(x0)+vec");
   }
 }
 

@@ -314,3 +314,17 @@ def test_snapshot_cadence():
     res = P.ncg.als_ncg_solve(R, cfg, snapshot=lambda m, it: seen.append((it, m.user_data[0])))
     assert [it for it, _ in seen] == [0, 2, 4, 6]
     assert seen[-1][1] == res.model.user_data[0]
+
+
+@pytest.mark.parametrize("n_f,seed", [(10, 0), (7, 12345), (100, 2**63 + 11)])
+def test_device_random_init_is_the_host_stream(n_f, seed):
+    # factors.cpp:24-32: x0 is generated on the device (mt19937_64 twists in
+    # one CTA); it must be bitwise the host Rng stream
+    T = random_ratings(37, 23, 0.3, 99)
+    R, _ = both(T)
+    cfg = P.SolverConfig(lambda_=0.1, n_f=n_f, max_iters=0, tol=0.0, seed=seed)
+    s = P.ncg.Solver(R, cfg)
+    m = s.model()
+    s.close()
+    want = P.random_init(n_f, T.n_u, T.n_m, seed)
+    assert np.array_equal(np.asarray(m), np.concatenate([want.user_data, want.item_data]))
