@@ -263,8 +263,8 @@ void launch_routing_count(DevRatings& R, int n_blocks, unsigned long long* d_out
 // the mt19937_64 stream of std::mt19937_64(seed) (state seeded on the host),
 // items first then users, u = (draw >> 11) * 2^-53 * (1/sqrt(n_f)) -- the
 // same operations as the host Rng::uniform, so x0 is bitwise the reference's.
-// One CTA walks the sequential twist chain (three barriers per 312-draw
-// block); the draws land straight in the padded flat vector.
+// One CTA walks the sequential twist chain (ping-pong state, two barriers
+// per 312-draw block); the draws land straight in the padded flat vector.
 namespace {
 constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull, kMtUpper = 0xFFFFFFFF80000000ull,
                    kMtLower = 0x000000007FFFFFFFull;
@@ -278,24 +278,22 @@ __global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restri
                                                           int64_t n_item_draws, int64_t n_draws,
                                                           int n_f, int ld, int n_u, double scale,
                                                           double* __restrict__ x) {
-  __shared__ uint64_t mt[312];
+  __shared__ uint64_t S[2][312];  // ping-pong state: two barriers per 312 draws
   const int tid = threadIdx.x;
-  if (tid < 312) mt[tid] = state0[tid];
+  if (tid < 312) S[0][tid] = state0[tid];
   __syncthreads();
+  int cur = 0;
   for (int64_t base = 0; base < n_draws; base += 312) {
-    uint64_t v = 0;
-    if (tid < 156) v = mt_twist(mt[tid], mt[tid + 1], mt[tid + 156]);
+    const int nx = cur ^ 1;
+    if (tid < 156) S[nx][tid] = mt_twist(S[cur][tid], S[cur][tid + 1], S[cur][tid + 156]);
     __syncthreads();
-    if (tid < 156) mt[tid] = v;
+    if (tid >= 156 && tid < 311) S[nx][tid] = mt_twist(S[cur][tid], S[cur][tid + 1], S[nx][tid - 156]);
+    if (tid == 311) S[nx][311] = mt_twist(S[cur][311], S[nx][0], S[nx][155]);
     __syncthreads();
-    if (tid >= 156 && tid < 311) v = mt_twist(mt[tid], mt[tid + 1], mt[tid - 156]);
-    if (tid == 311) v = mt_twist(mt[311], mt[0], mt[155]);
-    __syncthreads();
-    if (tid >= 156 && tid < 312) mt[tid] = v;
-    __syncthreads();
+    cur = nx;
     const int64_t k = base + tid;
     if (tid < 312 && k < n_draws) {
-      uint64_t z = mt[tid];
+      uint64_t z = S[cur][tid];
       z ^= (z >> 29) & 0x5555555555555555ull;
       z ^= (z << 17) & 0x71D67FFFEDA60000ull;
       z ^= (z << 37) & 0xFFF7EEE000000000ull;
@@ -330,8 +328,8 @@ void launch_random_init(Ctx* ctx, int n_f, int n_u, int n_m, uint64_t seed, doub
   k_mt_random_init<<<1, 320, 0, ctx->stream>>>(d, nm, nm + nu, n_f, ld, n_u,
                                                1.0 / std::sqrt(static_cast<double>(n_f)), x);
   ctx->end_launch(t);
-  // the host staging array must outlive the async copy
-  AB2_CUDA(cudaStreamSynchronize(ctx->stream));
+  // (no sync: a copy from pageable memory returns once `st` has been staged,
+  // so the host goes on to build the work plans while the chain runs)
 }
 
 }  // namespace ab2
