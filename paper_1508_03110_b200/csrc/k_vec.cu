@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restri
   if (tid < 312) S[0][tid] = state0[tid];
   __syncthreads();
   int cur = 0;
+  // draw k = base + tid -> (q, col) = divmod(k, n_f), kept incrementally (no
+  // 64-bit division in the chain): q < n_m are item rows, the rest user rows
+  int q = tid / n_f, col = tid % n_f;
+  const int dq = 312 / n_f, dc = 312 % n_f;
   for (int64_t base = 0; base < n_draws; base += 312) {
     const int nx = cur ^ 1;
     if (tid < 156) S[nx][tid] = mt_twist(S[cur][tid], S[cur][tid + 1], S[cur][tid + 156]);
@@ -300,15 +304,14 @@ __global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restri
       z ^= z >> 43;
       const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
       const double val = __dmul_rn(u, scale);
-      int64_t row, col;
-      if (k < n_item_draws) {
-        row = n_u + k / n_f;
-        col = k % n_f;
-      } else {
-        row = (k - n_item_draws) / n_f;
-        col = (k - n_item_draws) % n_f;
-      }
+      const int64_t row = k < n_item_draws ? n_u + q : q - (n_item_draws / n_f);
       x[row * ld + col] = val;
+    }
+    q += dq;
+    col += dc;
+    if (col >= n_f) {
+      col -= n_f;
+      ++q;
     }
   }
 }
