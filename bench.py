@@ -264,20 +264,43 @@ def run_gpu(args):
         res = _lib.ResultC()
         n = C.c_int(0)
         L = _lib.lib()
-        t0 = time.perf_counter()
-        h = C.c_void_p()
-        _lib.check(L.alsncg_ratings_upload(ctx.handle, R.n_users(), R.n_items(), R.nnz(),
-                                           *[C.c_void_p(t.data_ptr()) for t in host], C.byref(h)))
-        _lib.check(L.alsncg_ncg_solve(h, C.byref(ccfg), _lib.SNAPSHOT_FN(), None, C.byref(res),
-                                      C.c_void_p(model.data_ptr()), recs, e2e_iters + 2, C.byref(n)))
-        _lib.check(L.alsncg_ratings_free(h))
-        e2e_s = time.perf_counter() - t0
+
+        def one_call(cfg_c):
+            t0 = time.perf_counter()
+            h = C.c_void_p()
+            _lib.check(L.alsncg_ratings_upload(ctx.handle, R.n_users(), R.n_items(), R.nnz(),
+                                               *[C.c_void_p(t.data_ptr()) for t in host], C.byref(h)))
+            _lib.check(L.alsncg_ncg_solve(h, C.byref(cfg_c), _lib.SNAPSHOT_FN(), None, C.byref(res),
+                                          C.c_void_p(model.data_ptr()), recs, e2e_iters + 2, C.byref(n)))
+            _lib.check(L.alsncg_ratings_free(h))
+            return time.perf_counter() - t0
+
+        # warm-up call (first-use costs of this entry path), then three timed
+        # calls; the median is reported (host-side jitter on shared boxes)
+        one_call(P.SolverConfig(lambda_=lam, n_f=n_f, max_iters=1, tol=0.0, seed=0, paper_timing=True).to_c())
+        calls = sorted(one_call(ccfg) for _ in range(3))
+        e2e_s = calls[1]
         e2e = {"value": R.nnz() * e2e_iters / e2e_s, "unit": "ratings/s",
                "h2d_bytes_per_step": h2d / e2e_iters,
                "d2h_bytes_per_step": model.numel() * 8 / e2e_iters,
+               "call_seconds": calls,
                "note": (f"one alsncg_ratings_upload + alsncg_ncg_solve(max_iters={e2e_iters}) + model "
-                        f"download from pinned host buffers per measurement, incl. setup "
+                        f"download from pinned host buffers per measurement (median of 3 calls "
+                        f"after one untimed warm-up call), incl. setup "
                         f"(x0, gradient, P(x0)); bytes are per ALS-NCG iteration")}
+
+    # ---- time-to-tolerance (the metric's second half):
+    # (1/N)||g|| < 1e-6 on the same workload, paper_timing, device-resident
+    ttt = None
+    if world == 1 and not args.no_ttt:
+        tcfg = P.SolverConfig(lambda_=lam, n_f=n_f, max_iters=2000, tol=1e-6, seed=0,
+                              paper_timing=True, trace_every=1_000_000_000)
+        res = P.ncg.als_ncg_solve(R, tcfg, ctx=ctx)
+        last = res.trace.records[-1]
+        ttt = {"tol": 1e-6, "converged": bool(res.converged), "iterations": res.iterations,
+               "seconds": last.elapsed_seconds, "final_grad_norm": res.final_grad_norm,
+               "restarts": res.restarts, "note": "solve elapsed at the first k with (1/N)||g|| < tol "
+                                                 "(ncg.cpp:285-286), trace loss excluded"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -297,6 +320,7 @@ def run_gpu(args):
                            "n_f": n_f, "lambda": lam, "l2": "inputs > 126 MB L2 (no flush needed)",
                            "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
                 "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+                "time_to_tolerance": ttt,
                 "clocks": clk.summary(), "kernels": kernels,
                 "solver_state": {k: state[k] for k in ("iterations", "grad_norm", "restarts",
                                                        "fallback_steps")},
@@ -316,6 +340,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

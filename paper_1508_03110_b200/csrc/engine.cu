@@ -25,6 +25,20 @@ Ctx::Ctx(int dev) : device(dev) {
   AB2_CUDA(cudaMalloc(&d_scalars, sizeof(double) * 64));
   AB2_CUDA(cudaMemset(d_scalars, 0, sizeof(double) * 64));
   AB2_CUDA(cudaMallocHost(&h_scalars, sizeof(double) * 64));
+  cudaMemPool_t pool;
+  AB2_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;
+  AB2_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+}
+
+void* Ctx::alloc(size_t bytes) {
+  void* p = nullptr;
+  AB2_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), stream));
+  return p;
+}
+
+void Ctx::release(void* p) {
+  if (p) cudaFreeAsync(p, stream);
 }
 
 Ctx::~Ctx() {
@@ -189,9 +203,9 @@ void upload_view(Ctx* ctx, View& v, int row0, int row1, const int64_t* ptr, cons
   v.nnz = ptr[row1] - base;
   v.h_ptr.resize(v.nrows + 1);
   for (int r = 0; r <= v.nrows; ++r) v.h_ptr[r] = ptr[row0 + r] - base;
-  AB2_CUDA(cudaMalloc(&v.ptr, sizeof(int64_t) * (v.nrows + 1)));
-  AB2_CUDA(cudaMalloc(&v.idx, sizeof(int) * std::max<int64_t>(v.nnz, 1)));
-  AB2_CUDA(cudaMalloc(&v.val, sizeof(double) * std::max<int64_t>(v.nnz, 1)));
+  v.ptr = static_cast<int64_t*>(ctx->alloc(sizeof(int64_t) * (v.nrows + 1)));
+  v.idx = static_cast<int*>(ctx->alloc(sizeof(int) * std::max<int64_t>(v.nnz, 1)));
+  v.val = static_cast<double*>(ctx->alloc(sizeof(double) * std::max<int64_t>(v.nnz, 1)));
   AB2_CUDA(cudaMemcpyAsync(v.ptr, v.h_ptr.data(), sizeof(int64_t) * (v.nrows + 1),
                            cudaMemcpyHostToDevice, ctx->stream));
   if (v.nnz > 0) {
@@ -200,10 +214,10 @@ void upload_view(Ctx* ctx, View& v, int row0, int row1, const int64_t* ptr, cons
   }
 }
 
-void free_view(View& v) {
-  cudaFree(v.ptr);
-  cudaFree(v.idx);
-  cudaFree(v.val);
+void free_view(Ctx* ctx, View& v) {
+  ctx->release(v.ptr);
+  ctx->release(v.idx);
+  ctx->release(v.val);
   v.ptr = nullptr;
   v.idx = nullptr;
   v.val = nullptr;
@@ -233,8 +247,8 @@ DevRatings* upload_ratings(Ctx* ctx, int n_u, int n_m, int64_t nnz, const int64_
 
 DevRatings::~DevRatings() {
   if (ctx) cudaSetDevice(ctx->device);
-  free_view(users);
-  free_view(items);
+  free_view(ctx, users);
+  free_view(ctx, items);
   for (auto& m : plans)
     for (auto& kv : m) cudaFree(kv.second->block);
   for (auto& m : hs_plans)

@@ -93,6 +93,11 @@ struct Ctx {
   explicit Ctx(int dev);
   ~Ctx();
   void* scratch(int slot, size_t bytes);
+  // Stream-ordered allocations from the device pool (its release threshold
+  // is raised in the constructor, so per-solve / per-upload buffers are
+  // recycled instead of going through cudaMalloc/cudaFree every call).
+  void* alloc(size_t bytes);
+  void release(void* p);
   // Kernel launch bookkeeping: call before/after each launch.
   int begin_launch(const char* name);
   void end_launch(int token);

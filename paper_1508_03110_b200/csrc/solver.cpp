@@ -71,7 +71,7 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
   quartic_columns_ = 2 * tot.second;
   mark("routing");
   const int nbuf = ncg_ ? 10 : 2;
-  AB2_CUDA(cudaMalloc(&buf_, sizeof(double) * std::max<int64_t>(N_, 1) * nbuf));
+  buf_ = static_cast<double*>(ctx_->alloc(sizeof(double) * std::max<int64_t>(N_, 1) * nbuf));
   double* b = buf_;
   auto take = [&]() {
     double* p = b;
@@ -133,8 +133,7 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
 Solver::~Solver() {
   if (buf_) {
     cudaSetDevice(ctx_->device);
-    cudaStreamSynchronize(ctx_->stream);
-    cudaFree(buf_);
+    ctx_->release(buf_);  // stream-ordered: back to the pool after the last use
   }
 }
 

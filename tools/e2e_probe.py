@@ -9,7 +9,7 @@ L = _lib.lib()
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 host = [pin(R.uptr), pin(R.uidx), pin(R.uval), pin(R.iptr), pin(R.iidx), pin(R.ival)]
 model = torch.empty(100 * (R.n_users() + R.n_items()), dtype=torch.float64).pin_memory()
-for iters in (0, 1, 10, 10):
+for iters in (0, 1, 10, 10, 10, 10, 10, 10):
     ccfg = P.SolverConfig(lambda_=c["lam"], n_f=100, max_iters=max(iters, 1), tol=0.0, seed=0, paper_timing=True).to_c()
     recs = (_lib.TraceRecordC * (iters + 2))(); res = _lib.ResultC(); n = C.c_int(0)
     t0 = time.perf_counter(); h = C.c_void_p()
