@@ -110,9 +110,13 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
           *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
       }
     }
-    for (int t = gtid; t < C::CH; t += C::GT) {
+    for (int t = gtid; t < C::CH; t += C::GT) {  // rating values: async too (no stall on the load)
       const int rt = base + t;
-      g_smem[bo + t * C::LDS + ld] = rt < len ? a.val[beg + rt] : 0.0;
+      double* dst = &g_smem[bo + t * C::LDS + ld];
+      if (rt < len)
+        cp_async8(dst, a.val + beg + rt);
+      else
+        *dst = 0.0;
     }
   };
   int aoff[C::Q], boff[C::Q];

@@ -11,7 +11,8 @@ c = P.CONFIGS[cfg_idx]
 t = time.time(); R = P.generate(cfg_idx); print(f"generate {time.time()-t:.1f}s nnz={R.nnz()}", flush=True)
 ctx = P.default_context()
 t = time.time(); R.device(ctx); print(f"upload {time.time()-t:.2f}s", flush=True)
-cfg = P.SolverConfig(lambda_=c["lam"], n_f=n_f, max_iters=1000, tol=0.0, seed=0)
+cfg = P.SolverConfig(lambda_=c["lam"], n_f=n_f, max_iters=1000, tol=0.0, seed=0,
+                     trace_every=10**9 if os.environ.get("NO_TRACE") else 1)  # NO_TRACE: paper_timing-like
 t = time.time(); s = P.ncg.Solver(R, cfg); ctx.synchronize(); print(f"setup {time.time()-t:.2f}s", flush=True)
 s.step(1); ctx.synchronize()
 ctx.reset_stats(); ctx.set_profiling(True)
