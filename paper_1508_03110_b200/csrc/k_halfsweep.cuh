@@ -4,22 +4,21 @@
 //      (sum_t m_t m_t^T + lambda*n_c*I) u_c = sum_t r_t m_t ,  m_t = src row j_t
 // empty rows -> 0; unregularised or non-SPD systems -> least-norm solve.
 //
-// Design:
-//  * Rows are cut into segments of <= S ratings (SegPlan, heavy rows first).
-//    One group of GW warps owns a segment.  Gathered source rows are staged
-//    into shared memory with cp.async (16-byte, double-buffered, CH ratings
-//    per stage) as the augmented vector m' = [m, r] (rhs folded into the Gram).
-//  * Gram of m' on the FP64 tensor cores: mma.sync m8n8k4 f64 (SASS
-//    DMMA.8x8x4) over the NB(NB+1)/2 lower-triangular 8x8 blocks, k = 4
-//    ratings per MMA; block pairs are distributed round-robin over the warps,
-//    accumulators live in registers.
-//  * Single-segment rows finish in the same CTA: the Gram goes to shared
-//    memory, lambda*n_c is added to the diagonal and an in-place symmetric
-//    elimination (LDL^T form of Cholesky: a pivot <= 0 means "not SPD", as
-//    Eigen's LLT) runs on the augmented matrix, so the forward substitution
-//    falls out of the rhs row; one warp back-substitutes.
-//  * Multi-segment (heavy) rows write register partials per segment; a
-//    second kernel sums them in segment order (deterministic) and solves.
+// Design (K1-K4):
+//  * Rows are cut into segments of <= S ratings (heavy rows first); the
+//    Gram of the augmented vector m' = [m, r] (rhs folded in) is accumulated
+//    on the FP64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA.8x8x4) over the
+//    NB(NB+1)/2 lower-triangular 8x8 blocks.
+//  * Small ranks (NB <= 4): k_hs_main, one warp per segment -- cp.async
+//    staging, DMMA Gram, then the shifted symmetric elimination in shared
+//    memory (LDL^T; a pivot <= 0 means "not SPD", as Eigen's LLT); heavy rows
+//    write per-segment partials that k_hs_reduce sums in order and solves.
+//  * Larger ranks (split path): k_hs_gram_ws (persistent, warp-specialised:
+//    a TMA producer warp feeds a ring of stages, consumer warps own fixed
+//    block ranges) writes one partial Gram slot per segment;
+//    k_hs_slot_reduce folds heavy rows' slots in slot order; k_hs_solve_sw
+//    factors each column with a compile-time blocked schedule (one 4-warp CTA
+//    per column).  NB > 20 uses the non-persistent k_hs_gram.
 //  * Fallback columns (lambda*n_c == 0 or a non-positive pivot) are listed
 //    and solved by k_hs_fallback: exact reference-order Gram, cyclic Jacobi
 //    eigen-decomposition, pseudo-inverse solve + one refinement step

@@ -635,401 +635,13 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
 
 template <int NB>
 struct SolveCfg {
-  static constexpr int P = NB * (NB + 1) / 2;
-  static constexpr int PER_WARP = P * 64 + 2 * NB * 8;  // doubles: blocks + dinv + w
-  static constexpr int FIT = (220 * 1024) / (PER_WARP * 8);
-  static constexpr int WPB = FIT >= 8 ? 8 : (FIT < 1 ? 1 : FIT);
+  static constexpr int P = NB * (NB + 1) / 2;  // lower-triangular 8x8 blocks of the augmented Gram
 };
 
 __device__ __forceinline__ int pidx(int I, int J) { return I * (I + 1) / 2 + J; }
 // Swizzled 8x8 block storage: element (r, c) at 8r + (c ^ 4*((r>>1)&1)); the
 // C-fragment (16-byte) and A/B-fragment (8-byte) accesses are conflict-free.
 __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r >> 1) & 1))); }
-
-// K3: batched solve.  One warp per column: sums the column's partial Grams
-// (slot order) into a swizzled shared copy, adds lambda*n_c, then a
-// left-looking blocked LDL^T over 8-column block columns J:
-//   (1) C(I,J) -= sum_{K<J} L(I,K) * (D_K^-1 L(J,K))^T on the FP64 tensor
-//       cores, two block rows at a time (independent DMMA chains);
-//   (2) the 8x8 diagonal block is factored by lanes 0..7 (one row each);
-//   (3) the rows below are eliminated lane-parallel (TRSM form, 28 FMAs per
-//       row against the factored diagonal block).
-// Storage is unscaled (A(i,k) = L~(i,k) d_k) so the augmented rhs row is
-// eliminated with the matrix and forward substitution comes for free.
-template <int NB>
-__device__ __forceinline__ bool ldl_factor(double* M, double* dinv, int n_f, int lane) {
-  const int r = lane >> 2, q = lane & 3;
-  const int KP = (n_f + 7) / 8;
-  for (int J = 0; J < KP; ++J) {
-    // (1) updates from earlier panels, four block rows per pass (four
-    // independent DMMA accumulation chains)
-    if (J > 0) {
-      const double* bj = M + pidx(J, 0) * 64;
-      for (int I = J; I < NB; I += 4) {
-        double2 c[4];
-        const double* ap[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int Iu = min(I + u, NB - 1);
-          c[u] = *reinterpret_cast<const double2*>(M + pidx(Iu, J) * 64 + swz(r, 2 * q));
-          ap[u] = M + pidx(Iu, 0) * 64;
-        }
-        for (int K = 0; K < J; ++K) {
-          const int o = K * 64;
-          const double b0 = bj[o + swz(r, q)] * dinv[8 * K + q];
-          const double b1 = bj[o + swz(r, 4 + q)] * dinv[8 * K + 4 + q];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dmma884(c[u].x, c[u].y, -ap[u][o + swz(r, q)], b0);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dmma884(c[u].x, c[u].y, -ap[u][o + swz(r, 4 + q)], b1);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (I + u < NB) *reinterpret_cast<double2*>(M + pidx(I + u, J) * 64 + swz(r, 2 * q)) = c[u];
-      }
-      __syncwarp();
-    }
-    // (2) diagonal block: lane rr < 8 holds row rr of block (J,J)
-    double* D = M + pidx(J, J) * 64;
-    const int rr = lane & 7;
-    double row[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int k = 8 * J + c;
-      if (k >= n_f) {  // non-pivot columns (padding / rhs column)
-        if (lane == 0) dinv[k] = 0.0;
-        continue;
-      }
-      const double d = __shfl_sync(kFull, row[c], c);
-      if (!(d > 0.0)) return false;  // Eigen LLT: NumericalIssue on a non-positive pivot
-      const double inv = fast_rcp(d);
-      if (lane == 0) dinv[k] = inv;
-      const double l = row[c] * inv;
-#pragma unroll
-      for (int c2 = c + 1; c2 < 8; ++c2) {
-        const double a = __shfl_sync(kFull, row[c], c2);  // A(c2, c)
-        if (rr > c && c2 <= rr) row[c2] = fma(-l, a, row[c2]);
-      }
-    }
-    if (lane < 8)
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c <= rr) D[swz(rr, c)] = row[c];
-    __syncwarp();
-    // (3) rows below the diagonal block: x_c' -= x_c * A(c',c)/d_c
-    if (J + 1 < NB) {
-      double s[28];
-      {
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) s[t++] = D[swz(c2, c)] * dinv[8 * J + c];
-      }
-      for (int i = 8 * (J + 1) + lane; i < 8 * NB; i += 32) {
-        double* rowp = M + pidx(i >> 3, J) * 64;
-        const int ri = i & 7;
-        double x[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) x[c] = rowp[swz(ri, c)];
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], s[t++], x[c2]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) rowp[swz(ri, c)] = x[c];
-      }
-      __syncwarp();
-    }
-  }
-  return true;
-}
-
-template <int NB>
-__global__ void __launch_bounds__(SolveCfg<NB>::WPB * 32)
-    k_hs_solve(HsArgs a, SolveArgs s) {
-  using C = SolveCfg<NB>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rl = blockIdx.x * C::WPB + warp;
-  if (rl >= s.nrows) return;
-  const int lr = s.row0 + rl;
-  const int n_f = a.n_f, ld = a.ld;
-  double* M = g_smem + static_cast<size_t>(warp) * C::PER_WARP;
-  double* dinv = M + C::P * 64;
-  double* w = dinv + NB * 8;
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
-  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
-    for (int k = lane; k < ld; k += 32) out[k] = 0.0;
-    return;
-  }
-  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
-  if (!(shift > 0.0)) {
-    if (lane == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int r = lane >> 2, q = lane & 3;
-  {
-    const int ns = s.row_nslot[lr];
-    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
-    if (ns == 1) {
-      // one slot: bulk 16-byte async copies straight into the swizzled blocks
-#pragma unroll 8
-      for (int p = 0; p < C::P; ++p) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
-      cp_async_commit();
-      cp_async_wait<0>();
-    } else {
-      for (int p = 0; p < C::P; ++p) {  // heavy rows: sum slots in slot order
-        double2 v = *reinterpret_cast<const double2*>(base + p * 64);
-        for (int t = 1; t < ns; ++t) {
-          const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
-          v.x += u.x;
-          v.y += u.y;
-        }
-        *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
-      }
-    }
-    __syncwarp();
-    // lambda * n_c on the diagonal (als.cpp:58-59): lane (r, q) owns (r, 2q+e)
-#pragma unroll
-    for (int I = 0; I < NB; ++I)
-      if (8 * I + r < n_f && (r >> 1) == q) M[pidx(I, I) * 64 + swz(r, r)] += shift;
-  }
-  __syncwarp();
-  if (!ldl_factor<NB>(M, dinv, n_f, lane)) {
-    if (lane == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int KP = (n_f + 7) / 8;
-  // Back substitution: u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k, one
-  // 8-row panel at a time: the panel's 8 unknowns by shuffles in lanes 0..7,
-  // then every lane folds them into the remaining right-hand side.
-  const int IR = ld >> 3, rr = ld & 7;
-  for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
-  __syncwarp();
-  for (int K = KP - 1; K >= 0; --K) {
-    const int kc = 8 * K + (lane & 7);
-    double wk = (lane < 8 && kc < n_f) ? w[kc] : 0.0;
-    const double dk = (lane < 8 && kc < n_f) ? dinv[kc] : 0.0;
-#pragma unroll
-    for (int c = 7; c >= 0; --c) {
-      const double u = __shfl_sync(kFull, wk * dk, c);
-      if (lane < c) wk = fma(-M[pidx(K, K) * 64 + swz(c, lane)], u, wk);
-      if (lane == c) wk = u;
-    }
-    if (lane < 8 && kc < n_f) w[kc] = wk;
-    double uu[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) uu[c] = __shfl_sync(kFull, wk, c);
-    for (int i = lane; i < 8 * K; i += 32) {
-      const double* blk = M + pidx(K, i >> 3) * 64;
-      double acc = w[i];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (8 * K + c < n_f) acc = fma(-blk[swz(c, i & 7)], uu[c], acc);
-      w[i] = acc;
-    }
-    __syncwarp();
-  }
-  for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
-}
-
-// K3 (CTA form): one 4-warp CTA per column, right-looking blocked LDL^T.
-// Per 8-column panel J: (a) lanes 0..7 of warp 0 factor the diagonal block,
-// (b) all threads eliminate the panel rows below it (TRSM form), (c) the
-// four warps apply the panel to the trailing blocks with DMMA
-// (C(I,K) -= L(I,J) (D_J^-1 L(K,J))^T).  Back substitution by warp 0.
-constexpr int kSolveCtaWarps = 4;
-
-template <int NB>
-__global__ void __launch_bounds__(kSolveCtaWarps * 32) k_hs_solve_cta(HsArgs a, SolveArgs s) {
-  using C = SolveCfg<NB>;
-  constexpr int NT = kSolveCtaWarps * 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int lr = s.row0 + blockIdx.x;
-  const int n_f = a.n_f, ld = a.ld;
-  double* M = g_smem;
-  double* dinv = M + C::P * 64;
-  double* w = dinv + NB * 8;
-  __shared__ int fail;
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
-  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  if (count == 0) {
-    for (int k = tid; k < ld; k += NT) out[k] = 0.0;
-    return;
-  }
-  const double shift = a.lambda * static_cast<double>(count);
-  if (!(shift > 0.0)) {
-    if (tid == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int r = lane >> 2, q = lane & 3;
-  {
-    const int ns = s.row_nslot[lr];
-    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
-    if (ns == 1) {
-      for (int p = warp; p < C::P; p += kSolveCtaWarps) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
-      cp_async_commit();
-      cp_async_wait<0>();
-    } else {
-      for (int p = warp; p < C::P; p += kSolveCtaWarps) {
-        double2 v = *reinterpret_cast<const double2*>(base + p * 64);
-        for (int t = 1; t < ns; ++t) {
-          const double2 u = *reinterpret_cast<const double2*>(base + p * 64 + static_cast<int64_t>(t) * C::P * 64);
-          v.x += u.x;
-          v.y += u.y;
-        }
-        *reinterpret_cast<double2*>(M + p * 64 + swz(r, 2 * q)) = v;
-      }
-    }
-    if (tid == 0) fail = 0;
-    __syncthreads();
-    for (int k = tid; k < n_f; k += NT) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;
-    __syncthreads();
-  }
-  const int KP = (n_f + 7) / 8;
-  for (int J = 0; J < KP; ++J) {
-    double* D = M + pidx(J, J) * 64;
-    // (a) diagonal block
-    if (warp == 0) {
-      const int rr = lane & 7;
-      double row[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
-      bool ok = true;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int k = 8 * J + c;
-        if (k >= n_f) {
-          if (lane == 0) dinv[k] = 0.0;
-          continue;
-        }
-        const double d = __shfl_sync(kFull, row[c], c);
-        if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
-          ok = false;
-          break;
-        }
-        const double inv = fast_rcp(d);
-        if (lane == 0) dinv[k] = inv;
-        const double l = row[c] * inv;
-#pragma unroll
-        for (int c2 = c + 1; c2 < 8; ++c2) {
-          const double av = __shfl_sync(kFull, row[c], c2);
-          if (rr > c && c2 <= rr) row[c2] = fma(-l, av, row[c2]);
-        }
-      }
-      if (!ok) {
-        if (lane == 0) fail = 1;
-      } else if (lane < 8) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c <= rr) D[swz(rr, c)] = row[c];
-      }
-    }
-    __syncthreads();
-    if (fail) break;
-    // (b) rows below the diagonal block
-    if (J + 1 < NB) {
-      double sc[28];
-      {
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) sc[t++] = D[swz(c2, c)] * dinv[8 * J + c];
-      }
-      for (int i = 8 * (J + 1) + tid; i < 8 * NB; i += NT) {
-        double* rowp = M + pidx(i >> 3, J) * 64;
-        const int ri = i & 7;
-        double x[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) x[c] = rowp[swz(ri, c)];
-        int t = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], sc[t++], x[c2]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) rowp[swz(ri, c)] = x[c];
-      }
-    }
-    __syncthreads();
-    // (c) trailing update by panel J: block columns Kc in (J, KP), rows I in [Kc, NB)
-    if (J + 1 < KP) {
-      const double dk0 = dinv[8 * J + q], dk1 = dinv[8 * J + 4 + q];
-      for (int Kc = J + 1; Kc < KP; ++Kc) {
-        const double* bk = M + pidx(Kc, J) * 64;
-        const double b0 = bk[swz(r, q)] * dk0, b1 = bk[swz(r, 4 + q)] * dk1;
-        for (int I = Kc + warp; I < NB; I += 2 * kSolveCtaWarps) {
-          const int I2 = I + kSolveCtaWarps;
-          const bool two = I2 < NB;
-          const double* a0 = M + pidx(I, J) * 64;
-          const double* a1 = M + pidx(two ? I2 : I, J) * 64;
-          double* c0p = M + pidx(I, Kc) * 64 + swz(r, 2 * q);
-          double* c1p = M + pidx(two ? I2 : I, Kc) * 64 + swz(r, 2 * q);
-          double2 c0 = *reinterpret_cast<const double2*>(c0p);
-          double2 c1 = *reinterpret_cast<const double2*>(c1p);
-          dmma884(c0.x, c0.y, -a0[swz(r, q)], b0);
-          dmma884(c1.x, c1.y, -a1[swz(r, q)], b0);
-          dmma884(c0.x, c0.y, -a0[swz(r, 4 + q)], b1);
-          dmma884(c1.x, c1.y, -a1[swz(r, 4 + q)], b1);
-          *reinterpret_cast<double2*>(c0p) = c0;
-          if (two) *reinterpret_cast<double2*>(c1p) = c1;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (fail) {
-    if (tid == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  if (warp != 0) return;
-  // Back substitution (warp 0): u_k = (A[ld][k] - sum_{i>k} A[i][k] u_i) / d_k.
-  const int IR = ld >> 3, rr = ld & 7;
-  for (int k = lane; k < n_f; k += 32) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rr, k & 7)];
-  __syncwarp();
-  for (int K = KP - 1; K >= 0; --K) {
-    const int kc = 8 * K + (lane & 7);
-    double wk = (lane < 8 && kc < n_f) ? w[kc] : 0.0;
-    const double dk = (lane < 8 && kc < n_f) ? dinv[kc] : 0.0;
-#pragma unroll
-    for (int c = 7; c >= 0; --c) {
-      const double u = __shfl_sync(kFull, wk * dk, c);
-      if (lane < c) wk = fma(-M[pidx(K, K) * 64 + swz(c, lane)], u, wk);
-      if (lane == c) wk = u;
-    }
-    if (lane < 8 && kc < n_f) w[kc] = wk;
-    double uu[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) uu[c] = __shfl_sync(kFull, wk, c);
-    for (int i = lane; i < 8 * K; i += 32) {
-      const double* blk = M + pidx(K, i >> 3) * 64;
-      double acc = w[i];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (8 * K + c < n_f) acc = fma(-blk[swz(c, i & 7)], uu[c], acc);
-      w[i] = acc;
-    }
-    __syncwarp();
-  }
-  for (int k = lane; k < ld; k += 32) out[k] = k < n_f ? w[k] : 0.0;
-}
 
 // K3 (static-schedule form): one 4-warp CTA per column, right-looking blocked
 // LDL^T on the swizzled shared-memory block store, with the whole schedule
@@ -1419,14 +1031,9 @@ struct Mode {
 };
 
 constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
-constexpr bool kSolveCta = true;                  // CTA-per-column solve for n_f >= 63
 // compile-time kernel choice: only the kernels a rank uses are instantiated
 template <int NB>
 constexpr bool kGramWs = NB <= 20;                // warp-specialised persistent Gram
-template <int NB>
-constexpr bool kSolveCtaFor = kSolveCta && NB >= 9;
-template <int NB>
-constexpr bool kSolveSwFor = true;                // static-schedule CTA solve (k_hs_solve_sw)
 
 template <int NB>
 void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
@@ -1466,28 +1073,20 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       ctx->end_launch(tok);
     }
   } else {
-    using SC = SolveCfg<NB>;
     const size_t slot_bytes = sizeof(double) * C::P * 64;
     const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
     using GS = GramShape<NB>;
     using GC = HsCfg<NB, GS::W>;
     const size_t gsmem = sizeof(double) * std::max<size_t>(2 * kGramStage * GC::LDS + 2,
                                                            size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
-    const size_t ssmem = sizeof(double) * SC::PER_WARP * SC::WPB;
     static bool attr_set = false;
     if (!attr_set) {
       if constexpr (kGramWs<NB>)
         AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       else
         AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      if constexpr (kSolveSwFor<NB>) {
-        AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_sw<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(sizeof(double) * SwSched<NB, kSwWarps>::SMEM)));
-      } else if constexpr (kSolveCtaFor<NB>)  // exact size: the kernel also has static shared memory
-        AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_cta<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(sizeof(double) * SC::PER_WARP)));
-      else
-        AB2_CUDA(cudaFuncSetAttribute(k_hs_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_sw<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(double) * SwSched<NB, kSwWarps>::SMEM)));
       attr_set = true;
     }
     double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
@@ -1535,25 +1134,16 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       s.row_slot0 = P.row_slot0;
       s.row_nslot = P.row_nslot;
       s.G = G;
-      if constexpr (kSolveSwFor<NB>) {
-        if (b.multi1 > b.multi0) {  // the solve reads one (folded) slot per row
-          const int slot_d2 = C::P * 32;
-          const int64_t n = static_cast<int64_t>(b.multi1 - b.multi0) * slot_d2;
-          const int tok = ctx->begin_launch("halfsweep_slot_reduce");
-          k_hs_slot_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
-              P.multi_rows + b.multi0, b.multi1 - b.multi0, P.row_slot0, P.row_nslot, G, slot_d2);
-          ctx->end_launch(tok);
-        }
+      if (b.multi1 > b.multi0) {  // the solve reads one (folded) slot per row
+        const int slot_d2 = C::P * 32;
+        const int64_t n = static_cast<int64_t>(b.multi1 - b.multi0) * slot_d2;
+        const int tok = ctx->begin_launch("halfsweep_slot_reduce");
+        k_hs_slot_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
+            P.multi_rows + b.multi0, b.multi1 - b.multi0, P.row_slot0, P.row_nslot, G, slot_d2);
+        ctx->end_launch(tok);
       }
       const int tok = ctx->begin_launch("halfsweep_solve");
-      if constexpr (kSolveSwFor<NB>) {
-        k_hs_solve_sw<NB><<<s.nrows, kSwWarps * 32, sizeof(double) * SwSched<NB, kSwWarps>::SMEM, ctx->stream>>>(a, s);
-      } else if constexpr (kSolveCtaFor<NB>) {
-        const size_t csmem = sizeof(double) * SC::PER_WARP;
-        k_hs_solve_cta<NB><<<s.nrows, kSolveCtaWarps * 32, csmem, ctx->stream>>>(a, s);
-      } else {
-        k_hs_solve<NB><<<(s.nrows + SC::WPB - 1) / SC::WPB, SC::WPB * 32, ssmem, ctx->stream>>>(a, s);
-      }
+      k_hs_solve_sw<NB><<<s.nrows, kSwWarps * 32, sizeof(double) * SwSched<NB, kSwWarps>::SMEM, ctx->stream>>>(a, s);
       ctx->end_launch(tok);
     }
   }
