@@ -530,7 +530,7 @@ struct WsShape {
   }
   static constexpr int MAXP = max_pairs();
   static constexpr size_t smem_bytes() {
-    return sizeof(double) * STAGES * BUF + 2 * STAGES * sizeof(uint64_t);
+    return sizeof(double) * STAGES * BUF + 2 * STAGES * sizeof(uint64_t) + STAGES * sizeof(int);
   }
 };
 
@@ -551,19 +551,25 @@ template <int NB, int R>
 __device__ __forceinline__ void ws_consumer(const int* __restrict__ seg_len,
                                             const int* __restrict__ seg_slot, int n_seg,
                                             double* __restrict__ G, uint64_t* full,
-                                            uint64_t* empty, int lane) {
+                                            uint64_t* empty, const int* hdr, int lane) {
   using S = WsShape<NB>;
   constexpr int p0 = S::p_begin(R), np = S::p_begin(R + 1) - p0;
   const int lofs = (lane & 3) * S::LDS + (lane >> 2);
   int it = 0;
-  for (int seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+  for (;;) {
+    // the first stage of every segment carries the segment id (the producer
+    // takes segments from a global counter: dynamic, heavy-first balance)
+    int buf = it % S::STAGES;
+    mbar_wait(full + buf, (it / S::STAGES) & 1);
+    const int seg = hdr[buf];
+    if (seg >= n_seg) break;  // stop marker
     double acc[S::MAXP][2];
 #pragma unroll
     for (int p = 0; p < S::MAXP; ++p) acc[p][0] = acc[p][1] = 0.0;
     const int nst = (seg_len[seg] + kWsCH - 1) / kWsCH;
     for (int s = 0; s < nst; ++s, ++it) {
-      const int buf = it % S::STAGES;
-      mbar_wait(full + buf, (it / S::STAGES) & 1);
+      buf = it % S::STAGES;
+      if (s > 0) mbar_wait(full + buf, (it / S::STAGES) & 1);
       const int bo = buf * S::BUF + lofs;
 #pragma unroll
       for (int kk = 0; kk < kWsCH / 4; ++kk) ws_kstep<NB, R>(bo + kk * 4 * S::LDS, acc);
@@ -580,12 +586,14 @@ __device__ __forceinline__ void ws_consumer(const int* __restrict__ seg_len,
 template <int NB>
 __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
     k_hs_gram_ws(HsArgs a, const int* __restrict__ seg_len, const int64_t* __restrict__ seg_beg,
-                 const int* __restrict__ seg_slot, int n_seg, double* __restrict__ G) {
+                 const int* __restrict__ seg_slot, int n_seg, double* __restrict__ G,
+                 int* __restrict__ next_seg) {
   using S = WsShape<NB>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = a.ld;
   uint64_t* full = reinterpret_cast<uint64_t*>(g_smem + S::STAGES * S::BUF);
   uint64_t* empty = full + S::STAGES;
+  int* hdr = reinterpret_cast<int*>(empty + S::STAGES);  // segment id per stage
   // pad columns ld+1 .. LDS-1 stay zero for the whole kernel
   const int padw = S::LDS - ld - 1;
   for (int e = threadIdx.x; e < S::STAGES * kWsCH * padw; e += blockDim.x) {
@@ -602,13 +610,26 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
   __syncthreads();
   if (warp == S::GR) {  // ---------------- producer
     int it = 0;
-    for (int seg = blockIdx.x; seg < n_seg; seg += gridDim.x) {
+    for (;;) {
+      int seg = 0;
+      if (lane == 0) seg = atomicAdd(next_seg, 1);
+      seg = __shfl_sync(kFull, seg, 0);
+      if (seg >= n_seg) {  // publish a stop marker in the next stage
+        const int buf = it % S::STAGES, use = it / S::STAGES;
+        if (use > 0) mbar_wait(empty + buf, (use - 1) & 1);
+        if (lane == 0) {
+          hdr[buf] = n_seg;
+          mbar_arrive(full + buf);
+        }
+        break;
+      }
       const int len = seg_len[seg];
       const int64_t beg = seg_beg[seg];
       for (int base = 0; base < len; base += kWsCH, ++it) {
         const int buf = it % S::STAGES, use = it / S::STAGES;
         if (use > 0) mbar_wait(empty + buf, (use - 1) & 1);
         double* B = g_smem + buf * S::BUF;
+        if (lane == 0 && base == 0) hdr[buf] = seg;
         const int nv = min(kWsCH, len - base);
         const int t = lane;  // kWsCH == 32: one rating per lane
         B[t * S::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
@@ -627,7 +648,7 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
   // ------------------------------------------ consumers (compile-time band)
 #define AB2_WS(R)                                                                           \
   if (warp == R && R < S::GR)                                                               \
-    ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, lane);
+    ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, hdr, lane);
   AB2_WS(0) AB2_WS(1) AB2_WS(2) AB2_WS(3) AB2_WS(4) AB2_WS(5) AB2_WS(6) AB2_WS(7)
 #undef AB2_WS
 }
@@ -1110,9 +1131,11 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
             per_sm = std::max(per_sm, 1);
           }
           const int grid = std::min(nseg, per_sm * ctx->sm_count);  // persistent CTAs
+          int* next_seg = static_cast<int*>(ctx->scratch(8, sizeof(int)));
+          AB2_CUDA(cudaMemsetAsync(next_seg, 0, sizeof(int), ctx->stream));
           const int tok = ctx->begin_launch("halfsweep_gram");
           k_hs_gram_ws<NB><<<grid, (WS::GR + 1) * 32, WS::smem_bytes(), ctx->stream>>>(
-              a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G);
+              a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G, next_seg);
           ctx->end_launch(tok);
         }
       } else if (b.seg1 > b.seg0) {
