@@ -507,10 +507,10 @@ struct WsShape {
   static constexpr int GR = P < 2 ? 1 : ((P + 11) / 12 < 2 ? 2 : ((P + 11) / 12 > 8 ? 8 : (P + 11) / 12));
   static constexpr int LDS = NB * 8 + 4;
   static constexpr int BUF = kWsCH * LDS;
-  // ring depth: large ranks run more CTAs per SM on a 2-stage ring (more
-  // consumer warps keep the DMMA pipe fuller; measured 15.6 -> 15.3 ms at
-  // n_f = 100), small ranks keep 3 stages (gather latency dominates there)
-  static constexpr int STAGES = NB >= 12 ? 2 : 3;
+  // ring depth: 2 stages from NB = 6 up -- more CTAs per SM, more consumer
+  // warps on the DMMA pipe (measured 15.6 -> 15.3 ms at n_f = 100, Gram
+  // 4.87 -> 4.70 ms at n_f = 50); NB = 5 keeps 3 stages
+  static constexpr int STAGES = NB >= 6 ? 2 : 3;
   static constexpr int p_begin(int r) { return r * P / GR; }
   static constexpr int row_of(int p) {
     int i = 0;
