@@ -180,6 +180,87 @@ int orc_build(int n_u, int n_m, int64_t nnz, const int* users, const int* items,
   return 0;
 }
 
+/* ---------------------------------------------------- workload generator --
+ * BASELINE.json configs (SURVEY.md 8(d) "Synthetic generator"): the reference
+ * has no generator for these workloads, so this restates the recipe SURVEY.md
+ * 8(d) fixes, on the reference's own Rng draws (rng.cpp:36-58):
+ *   rank-10 truth u*, m* ~ sd*normal(), sd = 10^-1/4 (variance 1/sqrt(10));
+ *   per-user counts min + round(extra * exp(normal() - 1/2)) clamped to
+ *   [min, cap = max(min, n_m/2)], then +-1 passes in user order to hit nnz;
+ *   items ~ Zipf(1) via sample_cumulative (rng.cpp:51-58), repeats of the same
+ *   user redrawn (as data.cpp:250-264);
+ *   r = clamp(round(2*(3.5 + u*.m* + 0.5*normal()))/2, 0.5, 5.0), round half
+ *   away from zero (support.hpp:104).
+ * The product's alsncg_synth_generate must produce the same triples bit for
+ * bit (tests/test_golden.py); the bench's reference arm builds its input from
+ * this function so that it never loads the product library.
+ * Returns 0, or 1 on bad dimensions / unreachable nnz. */
+int orc_synth_generate(int n_u, int n_m, int64_t nnz, int min_per_user, uint64_t seed,
+                       int* users, int* items, double* values) {
+  enum { RANK = 10 };
+  if (n_u <= 0 || n_m <= 0 || min_per_user < 1 || min_per_user > n_m) return 1;
+  const int cap = min_per_user > n_m / 2 ? min_per_user : n_m / 2;
+  if (nnz < (int64_t)min_per_user * n_u || nnz > (int64_t)cap * n_u) return 1;
+  orc_rng rng;
+  orc_rng_seed(&rng, seed);
+  const double sd = pow(10.0, -0.25);
+  double* ut = (double*)malloc(sizeof(double) * (size_t)n_u * RANK);
+  double* mt = (double*)malloc(sizeof(double) * (size_t)n_m * RANK);
+  int* cnt = (int*)malloc(sizeof(int) * (size_t)n_u);
+  double* cum = (double*)malloc(sizeof(double) * (size_t)n_m);
+  int* stamp = (int*)malloc(sizeof(int) * (size_t)n_m);
+  for (int64_t k = 0; k < (int64_t)n_u * RANK; ++k) ut[k] = sd * orc_rng_normal(&rng);
+  for (int64_t k = 0; k < (int64_t)n_m * RANK; ++k) mt[k] = sd * orc_rng_normal(&rng);
+  const double extra = (double)nnz / n_u - min_per_user;
+  for (int i = 0; i < n_u; ++i) {
+    cnt[i] = min_per_user;
+    if (extra > 0.0) {
+      double c = min_per_user + round(extra * exp(orc_rng_normal(&rng) - 0.5));
+      if (c < min_per_user) c = min_per_user;
+      if (c > cap) c = cap;
+      cnt[i] = (int)c;
+    }
+  }
+  int64_t total = 0;
+  for (int i = 0; i < n_u; ++i) total += cnt[i];
+  int rc = 0;
+  while (total != nnz) {
+    int moved = 0;
+    for (int i = 0; i < n_u && total != nnz; ++i) {
+      if (total < nnz && cnt[i] < cap) { ++cnt[i]; ++total; moved = 1; }
+      else if (total > nnz && cnt[i] > min_per_user) { --cnt[i]; --total; moved = 1; }
+    }
+    if (!moved) { rc = 1; break; }
+  }
+  if (rc == 0) {
+    double run = 0.0;
+    for (int j = 0; j < n_m; ++j) { run += 1.0 / (double)(j + 1); cum[j] = run; stamp[j] = -1; }
+    int64_t pos = 0;
+    for (int i = 0; i < n_u; ++i) {
+      const double* u = ut + (size_t)i * RANK;
+      for (int drawn = 0; drawn < cnt[i];) {
+        const int j = orc_sample_cumulative(cum, n_m, orc_rng_uniform(&rng));
+        if (stamp[j] == i) continue;
+        stamp[j] = i;
+        ++drawn;
+        const double* m = mt + (size_t)j * RANK;
+        double score = 0.0;
+        for (int k = 0; k < RANK; ++k) score += u[k] * m[k];
+        const double eps = 0.5 * orc_rng_normal(&rng);
+        double r = round(2.0 * (3.5 + score + eps)) / 2.0;
+        if (r < 0.5) r = 0.5;
+        if (r > 5.0) r = 5.0;
+        users[pos] = i;
+        items[pos] = j;
+        values[pos] = r;
+        ++pos;
+      }
+    }
+  }
+  free(ut); free(mt); free(cnt); free(cum); free(stamp);
+  return rc;
+}
+
 /* ------------------------------------------------------------- factors -- */
 /* factors.cpp:24-32: items first, then users, U[0,1) * 1/sqrt(n_f). */
 void orc_random_init(int n_f, int n_u, int n_m, uint64_t seed, double* user, double* item) {

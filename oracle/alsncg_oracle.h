@@ -70,6 +70,11 @@ int orc_build(int n_u, int n_m, int64_t nnz, const int* users, const int* items,
               int64_t* uptr, int* uidx, double* uval,
               int64_t* iptr, int* iidx, double* ival, int* dup_user, int* dup_item);
 
+/* ---- BASELINE workload generator (restated recipe, no
+ * reference counterpart).  Returns 0 ok, 1 bad dimensions / nnz. */
+int orc_synth_generate(int n_u, int n_m, int64_t nnz, int min_per_user, uint64_t seed,
+                       int* users, int* items, double* values);
+
 /* ---- factors.cpp ---- */
 void orc_random_init(int n_f, int n_u, int n_m, uint64_t seed, double* user, double* item);
 /* FlatVector ops over (user part, item part) with nu = n_f*n_u, nm = n_f*n_m. */

@@ -85,6 +85,8 @@ def port():
                                   _lp, _ip, _dp, _lp, _ip, _dp, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int)]
         lib.orc_random_init.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, _dp, _dp]
+        lib.orc_synth_generate.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_uint64,
+                                           _ip, _ip, _dp]
         lib.orc_dot.argtypes = [C.c_int64, C.c_int64, _dp, _dp, _dp, _dp]
         lib.orc_dot.restype = C.c_double
         lib.orc_axpby.argtypes = [C.c_int64, C.c_int64, C.c_double, _dp, _dp, C.c_double,
@@ -362,6 +364,43 @@ class Oracle:
 
     def als_solve(self, R, cfg):
         return self._solve("als", R, cfg)
+
+
+# BASELINE.json workloads, restated on the oracle side (same table as the
+# product's synth.CONFIGS; tests/test_golden.py pins the two generators
+# bitwise) so that the reference arm never loads the product library.
+# index -> (n_users, n_items, nnz, n_f, lambda, data seed)
+CONFIGS = {
+    0: dict(n_u=1_000, n_m=500, nnz=20_000, n_f=10, lam=0.1, seed=1000),
+    1: dict(n_u=138_493, n_m=26_744, nnz=20_000_263, n_f=100, lam=0.01, seed=1001),
+    2: dict(n_u=138_493, n_m=26_744, nnz=20_000_263, n_f=(10, 25, 50, 100, 200), lam=0.01,
+            seed=1001),
+    3: dict(n_u=1_000_000, n_m=100_000, nnz=100_000_000, n_f=50, lam=0.05, seed=1003),
+    4: dict(n_u=8_000_000, n_m=800_000, nnz=960_000_000, n_f=25, lam=0.05, seed=1004),
+}
+
+
+def synth_triples(n_u, n_m, nnz, seed, min_per_user=20):
+    """orc_synth_generate: the BASELINE workload recipe."""
+    users = np.empty(nnz, np.int32)
+    items = np.empty(nnz, np.int32)
+    values = np.empty(nnz, np.float64)
+    if port().orc_synth_generate(n_u, n_m, nnz, min_per_user, seed, users, items, values):
+        raise ValueError("orc_synth_generate: bad dimensions or unreachable nnz")
+    return users, items, values
+
+
+def generate(config_index, scale_users=None):
+    """OracleRatings of BASELINE config `config_index` (optionally only the
+    first `scale_users` users' ratings, for bounded CPU samples)."""
+    c = CONFIGS[config_index]
+    users, items, values = synth_triples(c["n_u"], c["n_m"], c["nnz"], c["seed"])
+    n_u = c["n_u"]
+    if scale_users is not None and scale_users < n_u:
+        keep = users < scale_users
+        users, items, values = users[keep], items[keep], values[keep]
+        n_u = scale_users
+    return OracleRatings(n_u, c["n_m"], users, items, values)
 
 
 def dot(x, y):
