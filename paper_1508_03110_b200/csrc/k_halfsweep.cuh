@@ -16,9 +16,11 @@
 //  * Larger ranks (split path): k_hs_gram_ws (persistent, warp-specialised:
 //    a TMA producer warp feeds a ring of stages, consumer warps own fixed
 //    block ranges) writes one partial Gram slot per segment;
-//    k_hs_slot_reduce folds heavy rows' slots in slot order; k_hs_solve_sw
-//    factors each column with a compile-time blocked schedule (one 4-warp CTA
-//    per column).  NB > 20 uses the non-persistent k_hs_gram.
+//    k_hs_slot_reduce folds heavy rows' slots in slot order; k_hs_solve_ws
+//    (persistent, one CTA per SM, teams of four warps split by SM
+//    sub-partition: a pivot warp inverts the 8x8 diagonal blocks and runs the
+//    back substitution, three DMMA warps do the block TRSM and trailing
+//    updates) solves each column.  NB > 20 uses the non-persistent k_hs_gram.
 //  * Fallback columns (lambda*n_c == 0 or a non-positive pivot) are listed
 //    and solved by k_hs_fallback: exact reference-order Gram, cyclic Jacobi
 //    eigen-decomposition, pseudo-inverse solve + one refinement step

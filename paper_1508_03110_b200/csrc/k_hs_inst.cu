@@ -654,206 +654,214 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
 }
 
 
-template <int NB>
-struct SolveCfg {
-  static constexpr int P = NB * (NB + 1) / 2;  // lower-triangular 8x8 blocks of the augmented Gram
-};
-
 __device__ __forceinline__ int pidx(int I, int J) { return I * (I + 1) / 2 + J; }
 // Swizzled 8x8 block storage: element (r, c) at 8r + (c ^ 4*((r>>1)&1)); the
 // C-fragment (16-byte) and A/B-fragment (8-byte) accesses are conflict-free.
 __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r >> 1) & 1))); }
 
-// K3 (static-schedule form): one 4-warp CTA per column, right-looking blocked
-// LDL^T on the swizzled shared-memory block store, with the whole schedule
-// resolved at compile time (panel J, block coordinates and owning warp are
-// template constants, so the instruction stream is the arithmetic plus
-// immediate-offset shared loads/stores):
-//   F(J)  warp 0 factors the 8x8 diagonal block (lanes = rows, pivots by
-//         shuffle) and publishes 1/d and the 28 in-block coefficients;
-//   T(J)  one thread per row below the diagonal eliminates it against the
-//         block (TRSM form) and writes X = L~(I,J) and S = -X D^-1;
-//   U(J)  warps 1..3 apply C(I,K) += X_I S_K^T (two DMMAs per block,
-//         column-major chunks so S_K fragments are reused) while warp 0
-//         updates the next diagonal block and immediately factors it
-//         (F(J+1) overlaps the rest of U(J)).
-// Two CTA barriers per panel.  Back substitution by warp 0 as in k_hs_solve.
 template <int N, typename F>
 __device__ __forceinline__ void static_for(F&& f) {
   [&]<int... Is>(std::integer_sequence<int, Is...>) { (f(std::integral_constant<int, Is>{}), ...); }(
       std::make_integer_sequence<int, N>{});
 }
 
-constexpr int kSwWarps = 4;
-
-template <int NB, int W>
-struct SwSched {
+// ---------------------------------------------------------------------------
+// K3 v2 (k_hs_solve_ws): warp-specialised persistent solve.  One CTA per SM,
+// TEAMS teams of four warps, one column in flight per team (the team's
+// shared block store holds that column's lower-triangular augmented Gram).
+// The measured constraint (profiles/fp64_latency.txt): DFMA and DMMA share the
+// FP64 datapath of an SM sub-partition (SMSP), and a dependent scalar FP64
+// chain next to a warp streaming DMMAs waits ~87x its idle latency.  So the
+// roles are split by SMSP (warp w runs on SMSP w % 4):
+//   warp 4t   (SMSP 0, "pivot warp"): only the serial work -- the LDL^T
+//             pivots of each 8x8 diagonal block, done as an in-register
+//             Gauss-Jordan inverse (lanes hold the C-fragment layout), and
+//             the back substitution;
+//   warps 4t+1..4t+3 (SMSPs 1-3): only DMMA work -- per panel J
+//             Y'_I = -M(I,J) D_J^-1 (the TRSM as two DMMAs per block), then
+//             the trailing update M(I,K) += M(I,J) Y'_K^T; the owner of
+//             (J+1,J+1) updates it first and signals the pivot warp
+//             (lookahead), which inverts D_{J+1} while the rest of panel J's
+//             update runs.
+// Hand-offs use two mbarriers per team (pivot -> DMMA "inverse ready",
+// DMMA -> pivot "next diagonal updated") and a 96-thread named barrier
+// among the DMMA warps; no CTA-wide barrier after the prologue.  Blocked
+// elimination with explicit diagonal inverses: forward
+//   M(I,K) -= M(I,J) D_J^-1 M(K,J)^T  (I >= K > J, the rhs row included);
+// back substitution x_J = D_J^-1 (w_J - sum_{I>J} M(I,J)^T x_I), one 8x8
+// mat-vec per block instead of an 8-step chain.  A non-positive pivot (Eigen
+// LLT's NumericalIssue) sends the column to the least-norm fallback.
+template <int NB>
+struct WsSolve {
   static constexpr int P = NB * (NB + 1) / 2;
-  // U(J) blocks (I,K), J < K <= I < NB, column-major, without (J+1,J+1)
-  static constexpr int count(int J) { return (NB - 1 - J) * (NB - J) / 2 - 1; }
-  static constexpr int order(int J, int I, int K) {
-    return (K - 1 - J) * NB - ((K - 1) * K / 2 - J * (J + 1) / 2) + (I - K) - 1;
-  }
-  static constexpr int owner(int J, int I, int K) {
-    return (I == J + 1 && K == J + 1) ? 0 : 1 + order(J, I, K) * (W - 1) / count(J);
-  }
-  static constexpr int cidx(int c) { return c * 7 - c * (c - 1) / 2; }  // first coefficient of column c
-  // shared layout (doubles)
-  static constexpr int OFF_S = P * 64;             // NB blocks: -X D^-1 of the current panel
-  static constexpr int OFF_C = OFF_S + NB * 64;    // 28 TRSM coefficients (+4)
-  static constexpr int OFF_DINV = OFF_C + 32;      // NB*8
-  static constexpr int OFF_W = OFF_DINV + NB * 8;  // NB*8 back-substitution vector
-  static constexpr int SMEM = OFF_W + NB * 8;
+  static constexpr int OFF_S = P * 64;           // Y'_I staging, NB blocks
+  static constexpr int OFF_W = OFF_S + NB * 64;  // back-substitution vector, 8*NB
+  static constexpr int TEAM_D = OFF_W + NB * 8;  // doubles per team
+  static constexpr int TEAM_BYTES = TEAM_D * 8;
+  static constexpr int FIT = (227 * 1024) / TEAM_BYTES;
+  static constexpr int TEAMS = FIT > 6 ? 6 : (FIT < 1 ? 1 : FIT);
+  static constexpr int THREADS = TEAMS * 128;
 };
 
-// F(J): factor the diagonal block (warp 0): lane rr holds row rr (four
-// replicas per warp), pivots by shuffle.  Publishes the factored rows, 1/d
-// and the 28 in-block coefficients L(c2, c).  Returns false on a
-// non-positive pivot (uniform across the warp).
-template <int NB, int W, int J>
-__device__ __forceinline__ bool sw_factor(double* M, int n_f, int lane) {
-  using SS = SwSched<NB, W>;
-  double* D = M + pidx(J, J) * 64;
-  double* coef = M + SS::OFF_C;
-  double* dinv = M + SS::OFF_DINV;
-  const int rr = lane & 7;
-  __syncwarp();  // the block was just updated by this warp's lanes
-  double row[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) row[c] = D[swz(rr, c)];
-  bool ok = true;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int k = 8 * J + c;
-    double inv = 0.0;
-    if (k < n_f) {
-      const double d = __shfl_sync(kFull, row[c], c);
-      if (!(d > 0.0)) {  // Eigen LLT: NumericalIssue on a non-positive pivot
-        ok = false;
-        break;
-      }
-      inv = fast_rcp(d);
-      const double l = row[c] * inv;
-#pragma unroll
-      for (int c2 = c + 1; c2 < 8; ++c2) {
-        const double av = __shfl_sync(kFull, row[c], c2);  // A(c2, c)
-        if (rr > c && c2 <= rr) row[c2] = fma(-l, av, row[c2]);
-      }
-    }
-    if (lane == 0) dinv[k] = inv;
-    if (c < 7 && lane < 8 && rr > c) coef[SS::cidx(c) + rr - c - 1] = row[c] * inv;  // L(rr, c)
-  }
-  if (ok && lane < 8)
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c <= rr) D[swz(rr, c)] = row[c];
-  return ok;
-}
-
-// T(J): eliminate every row of the blocks below the diagonal (one per thread).
-
-template <int NB, int W, int J>
-__device__ __forceinline__ void sw_trsm_row(double* M, int row) {
-  using SS = SwSched<NB, W>;
-  const int I = J + 1 + (row >> 3), rr = row & 7;
-  const bool sw = (rr >> 1) & 1;  // swizzle: columns 0-3 and 4-7 swap halves
-  double2* xr = reinterpret_cast<double2*>(M + (I * (I + 1) / 2 + J) * 64 + 8 * rr);
-  double2* sr = reinterpret_cast<double2*>(M + SS::OFF_S + I * 64 + 8 * rr);
-  const double2* cf = reinterpret_cast<const double2*>(M + SS::OFF_C);
-  const double2* dv = reinterpret_cast<const double2*>(M + SS::OFF_DINV + 8 * J);
-  double x[8];
-  {
-    const double2 v0 = xr[0], v1 = xr[1], v2 = xr[2], v3 = xr[3];
-    x[0] = sw ? v2.x : v0.x; x[1] = sw ? v2.y : v0.y; x[2] = sw ? v3.x : v1.x; x[3] = sw ? v3.y : v1.y;
-    x[4] = sw ? v0.x : v2.x; x[5] = sw ? v0.y : v2.y; x[6] = sw ? v1.x : v3.x; x[7] = sw ? v1.y : v3.y;
-  }
-  double cc[28];
-#pragma unroll
-  for (int u = 0; u < 14; ++u) {
-    const double2 v = cf[u];
-    cc[2 * u] = v.x;
-    cc[2 * u + 1] = v.y;
-  }
-  {
-    int u = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-      for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], cc[u++], x[c2]);
-  }
-  double iv[8];
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const double2 v = dv[h];
-    iv[2 * h] = v.x;
-    iv[2 * h + 1] = v.y;
-  }
-  double s[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) s[c] = -x[c] * iv[c];
-  const int a = sw ? 2 : 0, b = sw ? 0 : 2;
-  xr[a] = make_double2(x[0], x[1]);
-  xr[a + 1] = make_double2(x[2], x[3]);
-  xr[b] = make_double2(x[4], x[5]);
-  xr[b + 1] = make_double2(x[6], x[7]);
-  sr[a] = make_double2(s[0], s[1]);
-  sr[a + 1] = make_double2(s[2], s[3]);
-  sr[b] = make_double2(s[4], s[5]);
-  sr[b + 1] = make_double2(s[6], s[7]);
-}
-
-template <int NB, int W, int J>
-__device__ __forceinline__ void sw_trsm(double* M, int tid) {
-  constexpr int ROWS = 8 * (NB - 1 - J);
-  for (int row = tid; row < ROWS; row += W * 32) sw_trsm_row<NB, W, J>(M, row);
-}
-
-// Compile-time list of the U(J) blocks warp w owns (column-major order).
-template <int NB, int W>
-struct SwList {
+// Compile-time work lists of DMMA warp d for panel J.
+template <int NB>
+struct WsList {
   int n;
   int I[NB * (NB + 1) / 2];
   int K[NB * (NB + 1) / 2];
-  static constexpr SwList make(int J, int w) {
-    SwList l{};
+  // Y' blocks: I in (J, NB) round-robin, I = J+1 on warp 0 (needed first)
+  static constexpr WsList y(int J, int d) {
+    WsList l{};
+    for (int i = J + 1; i < NB; ++i)
+      if ((i - J - 1) % 3 == d) {
+        l.I[l.n] = i;
+        l.K[l.n] = J;
+        ++l.n;
+      }
+    return l;
+  }
+  // update blocks (I,K), J < K <= I < NB: (J+1,J+1) is position 0 (warp 0,
+  // first); the rest in column-major order, split evenly over the 3 warps
+  static constexpr WsList u(int J, int d) {
+    WsList l{};
+    const int total = (NB - 1 - J) * (NB - J) / 2;
+    int pos = 0;
     for (int k = J + 1; k < NB; ++k)
-      for (int i = k; i < NB; ++i)
-        if (SwSched<NB, W>::owner(J, i, k) == w) {
+      for (int i = k; i < NB; ++i) {
+        const int p = (i == J + 1 && k == J + 1) ? 0 : ++pos;
+        if (p * 3 / total == d) {
           l.I[l.n] = i;
           l.K[l.n] = k;
           ++l.n;
         }
+      }
+    // (J+1,J+1) first within warp 0's list
+    for (int e = 1; e < l.n; ++e)
+      if (l.I[e] == J + 1 && l.K[e] == J + 1) {
+        const int ti = l.I[e], tk = l.K[e];
+        for (int f = e; f > 0; --f) {
+          l.I[f] = l.I[f - 1];
+          l.K[f] = l.K[f - 1];
+        }
+        l.I[0] = ti;
+        l.K[0] = tk;
+      }
     return l;
   }
 };
 
-template <int NB, int W, int J, int w>
-struct SwL {
-  static constexpr SwList<NB, W> v = SwList<NB, W>::make(J, w);
+template <int NB, int J, int d>
+struct WsY {
+  static constexpr WsList<NB> v = WsList<NB>::y(J, d);
+};
+template <int NB, int J, int d>
+struct WsU {
+  static constexpr WsList<NB> v = WsList<NB>::u(J, d);
 };
 
-// U(J) for warp w: C(I,K) += X_I S_K^T (S holds -X D^-1), G blocks at a time
-// with every load of a group issued before its DMMAs and stores (the
-// blocks are independent; the compiler cannot prove it through the lane
-// offsets, so the batching is explicit).
-template <int NB, int W, int J, int w>
-__device__ __forceinline__ void sw_update(double* M, int oc, int oa0, int oa1) {
-  using SS = SwSched<NB, W>;
-  using L = SwL<NB, W, J, w>;
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+// Pivot warp, panel J: Gauss-Jordan inverse of the (Schur-complemented)
+// diagonal block restricted to its nv valid pivots; writes -D^-1 (zero
+// outside nv x nv) over the block.  When the rhs row lives in this block
+// (J == IR) its first nv entries are saved to W first.  Returns false on a
+// non-positive (or NaN) pivot; the result is warp-uniform.
+template <int NB, int J, bool FULL>
+__device__ __forceinline__ bool ws_factor(double* M, int n_f, int IR, int rl, int lane) {
+  double* D = M + pidx(J, J) * 64;
+  double* W = M + WsSolve<NB>::OFF_W;
+  const int r = lane >> 2, q = lane & 3;
+  const int c0 = 2 * q, c1 = 2 * q + 1;
+  const double2 v = *reinterpret_cast<const double2*>(D + swz(r, c0));
+  double a0 = v.x, a1 = v.y;
+  const int nv = FULL ? 8 : min(8, n_f - 8 * J);  // FULL: all 8 pivots valid (no per-pivot branch)
+  if (J == IR && r == rl) {
+    W[8 * J + c0] = c0 < nv ? a0 : 0.0;
+    W[8 * J + c1] = c1 < nv ? a1 : 0.0;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (FULL || k < nv) {
+      const double p = __shfl_sync(kFull, (k & 1) ? a1 : a0, 4 * k + (k >> 1));
+      ok = ok && (p > 0.0);
+      const double ip = fast_rcp(p);
+      const double rk0 = __shfl_sync(kFull, a0, 4 * k + q) * ip;  // scaled row k at my columns
+      const double rk1 = __shfl_sync(kFull, a1, 4 * k + q) * ip;
+      const double ck = __shfl_sync(kFull, (k & 1) ? a1 : a0, 4 * r + (k >> 1));  // my row, column k
+      if (r == k) {
+        a0 = c0 == k ? ip : rk0;
+        a1 = c1 == k ? ip : rk1;
+      } else {
+        a0 = c0 == k ? -ck * ip : fma(-ck, rk0, a0);
+        a1 = c1 == k ? -ck * ip : fma(-ck, rk1, a1);
+      }
+    }
+  }
+  if (r >= nv) a0 = a1 = 0.0;
+  if (c0 >= nv) a0 = 0.0;
+  if (c1 >= nv) a1 = 0.0;
+  __syncwarp();
+  *reinterpret_cast<double2*>(D + swz(r, c0)) = make_double2(-a0, -a1);
+  return ok;
+}
+
+// DMMA warp d, panel J, step 1: Y'_I = M(I,J) (-D_J^-1) into the staging area.
+template <int NB, int J, int d>
+__device__ __forceinline__ void ws_y(double* M, int r, int q) {
+  using L = WsY<NB, J, d>;
+  if constexpr (L::v.n > 0) {
+    const double* ND = M + pidx(J, J) * 64;
+    const double b0 = ND[swz(q, r)], b1 = ND[swz(4 + q, r)];  // B[k][n] = ND[k][n]
+    static_for<L::v.n>([&](auto ic) {
+      constexpr int I = L::v.I[decltype(ic)::value];
+      const double* A = M + pidx(I, J) * 64;
+      double y0 = 0.0, y1 = 0.0;
+      dmma884(y0, y1, A[swz(r, q)], b0);
+      dmma884(y0, y1, A[swz(r, 4 + q)], b1);
+      *reinterpret_cast<double2*>(M + WsSolve<NB>::OFF_S + I * 64 + swz(r, 2 * q)) = make_double2(y0, y1);
+    });
+  }
+}
+
+// DMMA warp d, panel J, step 2: M(I,K) += M(I,J) Y'_K^T, four blocks per
+// batch (all loads first).  Warp 0 starts with (J+1,J+1) and then signals
+// the pivot warp through `upd`.
+template <int NB, int J, int d>
+__device__ __forceinline__ void ws_update(double* M, int r, int q, int lane, int KP, uint64_t* upd) {
+  using L = WsU<NB, J, d>;
+  constexpr int OS = WsSolve<NB>::OFF_S;
+  const int oc = swz(r, 2 * q), oa0 = swz(r, q), oa1 = swz(r, 4 + q);
+  auto one = [&](auto ic) {
+    constexpr int I = L::v.I[decltype(ic)::value], K = L::v.K[decltype(ic)::value];
+    double2 c = *reinterpret_cast<const double2*>(M + pidx(I, K) * 64 + oc);
+    dmma884(c.x, c.y, M[pidx(I, J) * 64 + oa0], M[OS + K * 64 + oa0]);
+    dmma884(c.x, c.y, M[pidx(I, J) * 64 + oa1], M[OS + K * 64 + oa1]);
+    *reinterpret_cast<double2*>(M + pidx(I, K) * 64 + oc) = c;
+  };
+  constexpr int first = (d == 0 && L::v.n > 0) ? 1 : 0;
+  if constexpr (first) {
+    one(std::integral_constant<int, 0>{});
+    __syncwarp();
+    if (J + 1 < KP && lane == 0) mbar_arrive(upd);
+  }
   constexpr int G = 4;
-  static_for<(L::v.n + G - 1) / G>([&](auto gc) {
-    constexpr int g0 = decltype(gc)::value * G;
+  constexpr int rest = L::v.n - first;
+  static_for<(rest + G - 1) / G>([&](auto gc) {
+    constexpr int g0 = first + decltype(gc)::value * G;
     double2 c[G];
     double xa[G][2], sb[G][2];
     static_for<G>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       if constexpr (g0 + i < L::v.n) {
         constexpr int I = L::v.I[g0 + i], K = L::v.K[g0 + i];
-        c[i] = *reinterpret_cast<const double2*>(M + (I * (I + 1) / 2 + K) * 64 + oc);
-        xa[i][0] = M[(I * (I + 1) / 2 + J) * 64 + oa0];
-        xa[i][1] = M[(I * (I + 1) / 2 + J) * 64 + oa1];
-        sb[i][0] = M[SS::OFF_S + K * 64 + oa0];
-        sb[i][1] = M[SS::OFF_S + K * 64 + oa1];
+        c[i] = *reinterpret_cast<const double2*>(M + pidx(I, K) * 64 + oc);
+        xa[i][0] = M[pidx(I, J) * 64 + oa0];
+        xa[i][1] = M[pidx(I, J) * 64 + oa1];
+        sb[i][0] = M[OS + K * 64 + oa0];
+        sb[i][1] = M[OS + K * 64 + oa1];
       }
     });
     static_for<G>([&](auto ic) {
@@ -868,152 +876,238 @@ __device__ __forceinline__ void sw_update(double* M, int oc, int oa0, int oa1) {
       constexpr int i = decltype(ic)::value;
       if constexpr (g0 + i < L::v.n) {
         constexpr int I = L::v.I[g0 + i], K = L::v.K[g0 + i];
-        *reinterpret_cast<double2*>(M + (I * (I + 1) / 2 + K) * 64 + oc) = c[i];
+        *reinterpret_cast<double2*>(M + pidx(I, K) * 64 + oc) = c[i];
       }
     });
   });
 }
 
-#ifdef AB2_SW_PROBE
-// development probe: per-phase clocks of the first 64 columns (warp 0, lane 0)
-__device__ unsigned long long g_sw_probe[64][64];
-#define SW_PROBE(slot) \
-  do { if ((blockIdx.x & 1023) == 0 && blockIdx.x < 65536 && (threadIdx.x & 127) == 0) g_sw_probe[blockIdx.x >> 10][slot] = clock64(); } while (0)
-#define SW_PROBE_W(slot) \
-  do { if ((blockIdx.x & 1023) == 0 && blockIdx.x < 65536 && (threadIdx.x & 31) == 0) g_sw_probe[blockIdx.x >> 10][slot] = clock64(); } while (0)
-#else
-#define SW_PROBE(slot) do {} while (0)
-#define SW_PROBE_W(slot) do {} while (0)
-#endif
-
-// The factorization proper for warp w; false if a pivot was non-positive.
-template <int NB, int W, int w>
-__device__ __forceinline__ bool sw_run(double* M, int n_f, int tid, int lane, volatile int* fail) {
-  using SS = SwSched<NB, W>;
-  const int KP = (n_f + 7) >> 3;
+template <int NB, int d>
+__device__ __forceinline__ void ws_dmma_role(double* M, int KP, int team, int lane, uint64_t* diag,
+                                             uint64_t* upd, unsigned& ph_diag, volatile int* fail,
+                                             unsigned long long* probe = nullptr) {
   const int r = lane >> 2, q = lane & 3;
-  const int oc = swz(r, 2 * q), oa0 = swz(r, q), oa1 = swz(r, 4 + q);
-  if constexpr (w == 0)
-    if (!sw_factor<NB, W, 0>(M, n_f, lane) && lane == 0) *fail = 1;
-  __syncthreads();
-  if (*fail) return false;
-  bool ok = true;
+  bool stop = false;
   static_for<NB>([&](auto Jc) {
     constexpr int J = decltype(Jc)::value;
-    if (!ok || J >= KP) return;
-    SW_PROBE(2 + 4 * J);
-    sw_trsm<NB, W, J>(M, tid);
-    SW_PROBE(3 + 4 * J);
-    __syncthreads();
-    if constexpr (J + 1 < NB) {
-      // (blocks of column NB-1 are updated even when it is not a pivot
-      // column: harmless, they are never read again)
-      SW_PROBE(4 + 4 * J);
-      sw_update<NB, W, J, w>(M, oc, oa0, oa1);
-      if constexpr (w == 0) {
-        SW_PROBE_W(5 + 4 * J);
-        if (J + 1 < KP && !sw_factor<NB, W, J + 1>(M, n_f, lane) && lane == 0) *fail = 1;
-      }
+    if (stop || J >= KP) return;
+    mbar_wait(diag, ph_diag & 1);
+    ++ph_diag;
+    if (*fail) {
+      stop = true;
+      return;
     }
-    __syncthreads();
-    if (*fail) ok = false;
+    if constexpr (J + 1 < NB) {
+      ws_y<NB, J, d>(M, r, q);
+      named_bar(1 + team, 96);
+      ws_update<NB, J, d>(M, r, q, lane, KP, upd);
+      named_bar(1 + team, 96);
+      if (probe && lane == 0 && J < 19) probe[4 + 3 * J] = clock64();
+    }
   });
-  return ok;
 }
 
+#ifdef AB2_WS_PROBE
+// development probe: phase clocks of the first column of team 0 in CTAs 0..63
+__device__ unsigned long long g_ws_probe[64][64];
+#define WS_PROBE(slot) \
+  do { if (probe_on && lane == 0) g_ws_probe[blockIdx.x][slot] = clock64(); } while (0)
+#define WS_PROBE_V(slot, v) \
+  do { if (probe_on && lane == 0) g_ws_probe[blockIdx.x][slot] = (v); } while (0)
+#else
+#define WS_PROBE(slot) do {} while (0)
+#define WS_PROBE_V(slot, v) do {} while (0)
+#endif
+
 template <int NB>
-__global__ void __launch_bounds__(kSwWarps * 32) k_hs_solve_sw(HsArgs a, SolveArgs s) {
-  using C = SolveCfg<NB>;
-  using SS = SwSched<NB, kSwWarps>;
-  constexpr int NT = kSwWarps * 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  SW_PROBE(0);
-  const int lr = s.row0 + blockIdx.x;
-  const int n_f = a.n_f, ld = a.ld;
-  double* M = g_smem;
-  double* dinv = M + SS::OFF_DINV;
-  double* w = M + SS::OFF_W;
-  __shared__ int fail;
-  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
-  const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
-    for (int k = tid; k < ld; k += NT) out[k] = 0.0;
-    return;
-  }
-  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
-  if (!(shift > 0.0)) {
-    if (tid == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  const int r = lane >> 2, q = lane & 3;
+__global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
+    k_hs_solve_ws(HsArgs a, SolveArgs s, int* __restrict__ next_col) {
+  using W = WsSolve<NB>;
+  constexpr int T = W::TEAMS;
+  __shared__ uint64_t bars[T][2];  // [0] inverse ready (pivot -> DMMA), [1] next diagonal updated
+  __shared__ int team_col[T];
+  __shared__ int team_fail[T];
+  __shared__ int slot_of[T * 4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Roles by SM sub-partition: the warp's hardware slot (%warpid) decides its
+  // SMSP (slot % 4), not its index in the CTA (measured: CTA warp 0 lands on
+  // slots 1..3).  When the CTA's warps are spread evenly (T per SMSP), the
+  // warps on SMSP 0 become the pivot warps and team t takes the t-th warp of
+  // every SMSP; otherwise fall back to index order.
   {
-    // heavy rows were folded into their first slot by k_hs_slot_reduce
-    const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * C::P * 64 + lane * 2;
-    for (int p = warp; p < C::P; p += kSwWarps) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
-    cp_async_commit();
-    cp_async_wait<0>();
-    if (tid == 0) fail = 0;
-    __syncthreads();
-    for (int k = tid; k < n_f; k += NT) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;  // als.cpp:58-59
-    __syncthreads();
-  }
-  SW_PROBE(1);
-  bool ok;
-  switch (warp) {
-    case 0: ok = sw_run<NB, kSwWarps, 0>(M, n_f, tid, lane, &fail); break;
-    case 1: ok = sw_run<NB, kSwWarps, 1>(M, n_f, tid, lane, &fail); break;
-    case 2: ok = sw_run<NB, kSwWarps, 2>(M, n_f, tid, lane, &fail); break;
-    default: ok = sw_run<NB, kSwWarps, 3>(M, n_f, tid, lane, &fail); break;
-  }
-  if (!ok) {
-    if (tid == 0) {
-      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
-      atomicAdd(a.fb_total, 1u);
-    }
-    return;
-  }
-  SW_PROBE(60);
-  // Back substitution, all warps: u_k = (w_k - sum_{i>k} A~(i,k) u_i) / d_k,
-  // one 8-row block at a time: every thread solves the block's 8 unknowns
-  // from registers (same arithmetic in every thread), then thread i < 8K
-  // folds them into w_i.
-  const int KP = (n_f + 7) >> 3;
-  {
-    const int IR = ld >> 3, rl = ld & 7;
-    for (int k = tid; k < n_f; k += NT) w[k] = M[pidx(IR, k >> 3) * 64 + swz(rl, k & 7)];
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    if (lane == 0) slot_of[warp] = static_cast<int>(wid);
   }
   __syncthreads();
-  for (int K = KP - 1; K >= 0; --K) {
-    const double* D = M + pidx(K, K) * 64;
-    double u[8];
-#pragma unroll
-    for (int c = 7; c >= 0; --c) {
-      double v = 0.0;
-      if (8 * K + c < n_f) {
-        v = w[8 * K + c];
-#pragma unroll
-        for (int i = 7; i > c; --i) v = fma(-D[swz(i, c)], u[i], v);  // u[c+1] (latest) last
-        v *= dinv[8 * K + c];
+  int team = warp >> 2, role = warp & 3;
+  {
+    int cnt[4] = {0, 0, 0, 0}, my_s = 0, my_rank = 0;
+    for (int w = 0; w < T * 4; ++w) {
+      const int sp = slot_of[w] & 3;
+      if (w == warp) {
+        my_s = sp;
+        my_rank = cnt[sp];
       }
-      u[c] = v;
+      ++cnt[sp];
     }
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (tid == c && 8 * K + c < n_f) out[8 * K + c] = u[c];
-    for (int i = tid; i < 8 * K; i += NT) {
-      const double* blk = M + pidx(K, i >> 3) * 64;
-      double acc = w[i];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc = fma(-blk[swz(c, i & 7)], u[c], acc);
-      w[i] = acc;
+    if (cnt[0] == T && cnt[1] == T && cnt[2] == T && cnt[3] == T) {
+      team = my_rank;
+      role = my_s;
     }
-    __syncthreads();
   }
-  for (int k = n_f + tid; k < ld; k += NT) out[k] = 0.0;
-  SW_PROBE(61);
+  const int ttid = role * 32 + lane;
+  double* M = g_smem + static_cast<size_t>(team) * W::TEAM_D;
+  double* Wv = M + W::OFF_W;
+  const int n_f = a.n_f, ld = a.ld;
+  const int KP = (n_f + 7) >> 3;
+  const int IR = ld >> 3, rl = ld & 7;
+  const int r = lane >> 2, q = lane & 3;
+  const int team_bar = 1 + T + team;
+  if (ttid == 0) {
+    mbar_init(&bars[team][0], 1);
+    mbar_init(&bars[team][1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  unsigned ph_diag = 0, ph_upd = 0;
+#ifdef AB2_WS_PROBE
+  bool probe_on = team == 0 && blockIdx.x < 64;
+  if (probe_on && lane == 0) {
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    g_ws_probe[blockIdx.x][62 + (role > 0)] = wid;  // SMSP = warpid % 4
+  }
+#endif
+  for (;;) {
+    named_bar(team_bar, 128);  // the previous column's smem reads are done
+    if (ttid == 0) {
+      team_col[team] = atomicAdd(next_col, 1);
+      team_fail[team] = 0;
+    }
+    named_bar(team_bar, 128);
+    const int c = team_col[team];
+    if (c >= s.nrows) break;
+    if (role == 0) WS_PROBE(0);
+    const int lr = s.row0 + c;
+    double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+    const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
+    if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
+      for (int k = ttid; k < ld; k += 128) out[k] = 0.0;
+      continue;
+    }
+    const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
+    if (!(shift > 0.0)) {
+      if (ttid == 0) {
+        a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+        atomicAdd(a.fb_total, 1u);
+      }
+      continue;
+    }
+    {  // heavy rows were folded into their first slot by k_hs_slot_reduce
+      const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * W::P * 64 + lane * 2;
+      for (int p = role; p < W::P; p += 4) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    named_bar(team_bar, 128);
+    if (role == 0) WS_PROBE(1);
+    if (role == 0) {
+      for (int k = lane; k < n_f; k += 32) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;  // als.cpp:58-59
+      __syncwarp();
+      bool ok = true;
+      static_for<NB>([&](auto Jc) {
+        constexpr int J = decltype(Jc)::value;
+        if (!ok || J >= KP) return;
+        if (J > 0) {
+          mbar_wait(&bars[team][1], ph_upd & 1);
+          ++ph_upd;
+        }
+        if (J < 19) WS_PROBE(2 + 3 * J);
+        ok = 8 * (J + 1) <= n_f ? ws_factor<NB, J, true>(M, n_f, IR, rl, lane)
+                                : ws_factor<NB, J, false>(M, n_f, IR, rl, lane);
+        if (J < 19) WS_PROBE(3 + 3 * J);
+        if (!ok && lane == 0) team_fail[team] = 1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[team][0]);
+        ++ph_diag;
+      });
+    } else if (role == 1) {
+#ifdef AB2_WS_PROBE
+      ws_dmma_role<NB, 0>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team],
+                          probe_on ? &g_ws_probe[blockIdx.x][0] : nullptr);
+#else
+      ws_dmma_role<NB, 0>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
+#endif
+    } else if (role == 2) {
+      ws_dmma_role<NB, 1>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
+    } else {
+      ws_dmma_role<NB, 2>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
+    }
+    named_bar(team_bar, 128);  // every panel of this column is done
+    if (role == 0) WS_PROBE(60);
+    if (team_fail[team]) {
+      if (ttid == 0) {
+        a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+        atomicAdd(a.fb_total, 1u);
+      }
+      continue;
+    }
+#ifdef AB2_WS_PROBE
+    if (role != 0) probe_on = false;
+#endif
+    if (role != 0) continue;
+    // ---- back substitution (pivot warp), x_J = D_J^-1 (w_J - sum_{I>J} M(I,J)^T x_I)
+    // w lives in registers: lane l owns entries l + 32u.  Per block J:
+    // gather w_J by shuffle, x_J[n] = -(ND_J w_J)[n] in lane n (two 4-term
+    // chains), broadcast x_J, fold it into the owned entries of blocks K < J.
+    constexpr int NWR = (8 * NB + 31) / 32;
+    double wr[NWR];
+#pragma unroll
+    for (int u = 0; u < NWR; ++u) {
+      const int i = lane + 32 * u;
+      const int K = i >> 3;
+      wr[u] = i < 8 * KP ? (K < IR ? M[pidx(IR, K) * 64 + swz(rl, i & 7)] : Wv[i]) : 0.0;
+    }
+    for (int J = KP - 1; J >= 0; --J) {
+      const int u = J >> 2;  // entries 8J..8J+7 sit in register u of lanes (8J & 31)..+7
+      double wsrc = wr[0];
+#pragma unroll
+      for (int v = 1; v < NWR; ++v) wsrc = u == v ? wr[v] : wsrc;
+      const double* ND = M + pidx(J, J) * 64;
+      const int n = lane & 7;
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        t0 = fma(ND[swz(n, cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + cc), t0);
+        t1 = fma(ND[swz(n, 4 + cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + 4 + cc), t1);
+      }
+      const double x = -(t0 + t1);
+      if (lane < 8 && 8 * J + n < n_f) out[8 * J + n] = x;
+      double xr[8];
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) xr[rr] = __shfl_sync(kFull, x, rr);
+#pragma unroll
+      for (int v = 0; v < NWR; ++v) {
+        const int i = lane + 32 * v;
+        if (i < 8 * J) {
+          const double* blk = M + pidx(J, i >> 3) * 64;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            a0 = fma(blk[swz(rr, i & 7)], xr[rr], a0);
+            a1 = fma(blk[swz(4 + rr, i & 7)], xr[4 + rr], a1);
+          }
+          wr[v] -= a0 + a1;
+        }
+      }
+    }
+    for (int k = n_f + lane; k < ld; k += 32) out[k] = 0.0;
+    WS_PROBE(61);
+#ifdef AB2_WS_PROBE
+    probe_on = false;
+#endif
+  }
 }
 
 // Heavy rows: fold a row's partial Gram slots into its first slot, in slot
@@ -1106,8 +1200,8 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
         AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       else
         AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_sw<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(double) * SwSched<NB, kSwWarps>::SMEM)));
+      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    WsSolve<NB>::TEAMS * WsSolve<NB>::TEAM_BYTES));
       attr_set = true;
     }
     double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
@@ -1165,8 +1259,12 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
             P.multi_rows + b.multi0, b.multi1 - b.multi0, P.row_slot0, P.row_nslot, G, slot_d2);
         ctx->end_launch(tok);
       }
+      int* next_col = static_cast<int*>(ctx->scratch(9, sizeof(int)));
+      AB2_CUDA(cudaMemsetAsync(next_col, 0, sizeof(int), ctx->stream));
+      using WSV = WsSolve<NB>;
+      const int grid = std::min(s.nrows, ctx->sm_count);  // persistent: one CTA per SM
       const int tok = ctx->begin_launch("halfsweep_solve");
-      k_hs_solve_sw<NB><<<s.nrows, kSwWarps * 32, sizeof(double) * SwSched<NB, kSwWarps>::SMEM, ctx->stream>>>(a, s);
+      k_hs_solve_ws<NB><<<grid, WSV::THREADS, WSV::TEAMS * WSV::TEAM_BYTES, ctx->stream>>>(a, s, next_col);
       ctx->end_launch(tok);
     }
   }
@@ -1182,10 +1280,10 @@ void run_hs<AB2_HS_NB>(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
 }  // namespace hs
 }  // namespace ab2
 
-#ifdef AB2_SW_PROBE
+#ifdef AB2_WS_PROBE
 #define AB2_CAT2(a, b) a##b
 #define AB2_CAT(a, b) AB2_CAT2(a, b)
-extern "C" int AB2_CAT(alsncg_debug_sw_probe_, AB2_HS_NB)(unsigned long long* out) {
-  return static_cast<int>(cudaMemcpyFromSymbol(out, ab2::hs::g_sw_probe, sizeof(ab2::hs::g_sw_probe)));
+extern "C" int AB2_CAT(alsncg_debug_ws_probe_, AB2_HS_NB)(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, ab2::hs::g_ws_probe, sizeof(ab2::hs::g_ws_probe)));
 }
 #endif
