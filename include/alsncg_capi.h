@@ -133,6 +133,25 @@ int alsncg_ctx_create(int device, alsncg_ctx** out);
 int alsncg_nccl_unique_id(unsigned char id[128]);
 int alsncg_ctx_create_dist(int device, int rank, int world, const unsigned char id[128],
                            alsncg_ctx** out);
+/* Trace CSV of one run (harness.cpp:80-118: header
+ * "iter,loss,grad_norm,elapsed_s,backtracks,shuffled_columns", %.17g doubles;
+ * the restarted flag is not part of the file).  read returns the record count
+ * in *n and fills min(*n, cap) records; ALSNCG_EDATA on unreadable / malformed
+ * files, ALSNCG_ELOGIC on out-of-order iterations. */
+int alsncg_write_trace_csv(const char* path, const alsncg_trace_record* recs, int n);
+int alsncg_read_trace_csv(const char* path, alsncg_trace_record* recs, int cap, int* n);
+
+/* Testing aid (no reference counterpart): an in-process stand-in for the NCCL
+ * communicator.  `world` contexts on one or more devices of ONE process, each
+ * driven by its own host thread, exchange factor shards and scalar partials
+ * through device-to-device copies; every collective drains all ranks' streams
+ * first, so the sharded code path runs end to end with its GPU work serialised
+ * (used by the -m gpu tests to check world = 2 against world = 1 bitwise on a
+ * single GPU). */
+typedef struct alsncg_loopgroup alsncg_loopgroup;
+int alsncg_loopgroup_create(int world, alsncg_loopgroup** out);
+int alsncg_loopgroup_destroy(alsncg_loopgroup* group);
+int alsncg_ctx_create_loopback(int device, int rank, alsncg_loopgroup* group, alsncg_ctx** out);
 int alsncg_ctx_destroy(alsncg_ctx* ctx);
 int alsncg_ctx_info(alsncg_ctx* ctx, int* device, int* rank, int* world);
 /* The cudaStream_t (as void*) every kernel of this context is launched on. */

@@ -12,6 +12,8 @@
 #include "alsncg/als.hpp"
 #include "alsncg/config.hpp"
 #include "alsncg/factors.hpp"
+#include "alsncg/harness.hpp"
+#include "alsncg/ranking.hpp"
 #include "alsncg/linesearch.hpp"
 #include "alsncg/ncg.hpp"
 #include "alsncg/parallel.hpp"
@@ -229,3 +231,37 @@ int ref_als_solve(void* h, const orc_config* cfg, double* mu, double* mm, orc_tr
 }
 
 }  // extern "C"
+
+// ---- off-path pins: trace CSV (harness.cpp:80-118) and ranking evaluation
+// (ranking.cpp:40-109), through the reference's own functions.
+extern "C" int ref_write_trace_csv(const char* path, int n, const int* iter, const double* loss,
+                                   const double* grad_norm, const double* elapsed, const int* backtracks,
+                                   const long long* shuffled) {
+  try {
+    ConvergenceTrace t;
+    for (int i = 0; i < n; ++i) {
+      TraceRecord r;
+      r.iter = iter[i];
+      r.loss = loss[i];
+      r.grad_norm = grad_norm[i];
+      r.elapsed_seconds = elapsed[i];
+      r.backtracks = backtracks[i];
+      r.shuffled_columns = shuffled[i];
+      t.records.push_back(r);
+    }
+    harness::write_trace_csv(path, t);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
+extern "C" double ref_mean_ranking_accuracy(int n_f, int n_u, int n_m, const double* uk, const double* mk,
+                                            const double* uf, const double* mf, int t, int n_workers) {
+  FactorModel a(n_f, n_u, n_m), b(n_f, n_u, n_m);
+  std::memcpy(a.user_data.data(), uk, sizeof(double) * a.user_data.size());
+  std::memcpy(a.item_data.data(), mk, sizeof(double) * a.item_data.size());
+  std::memcpy(b.user_data.data(), uf, sizeof(double) * b.user_data.size());
+  std::memcpy(b.item_data.data(), mf, sizeof(double) * b.item_data.size());
+  return ranking::mean_ranking_accuracy(a, b, t, n_workers);
+}

@@ -56,6 +56,11 @@ SIGNATURES = {
     "alsncg_ctx_create": (i32, [i32, C.POINTER(vp)]),
     "alsncg_nccl_unique_id": (i32, [vp]),
     "alsncg_ctx_create_dist": (i32, [i32, i32, i32, vp, C.POINTER(vp)]),
+    "alsncg_loopgroup_create": (i32, [i32, C.POINTER(vp)]),
+    "alsncg_write_trace_csv": (i32, [C.c_char_p, vp, i32]),
+    "alsncg_read_trace_csv": (i32, [C.c_char_p, vp, i32, ip]),
+    "alsncg_loopgroup_destroy": (i32, [vp]),
+    "alsncg_ctx_create_loopback": (i32, [i32, i32, vp, C.POINTER(vp)]),
     "alsncg_ctx_destroy": (i32, [vp]),
     "alsncg_ctx_info": (i32, [vp, ip, ip, ip]),
     "alsncg_ctx_stream": (vp, [vp]),

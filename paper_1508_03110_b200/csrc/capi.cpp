@@ -5,6 +5,8 @@
 #include <string>
 #include <vector>
 
+#include "alsncg/harness.hpp"
+#include "alsncg/ratings.hpp"
 #include "alsncg_capi.h"
 #include "engine.h"
 #include "host_data.h"
@@ -36,6 +38,20 @@ int guarded(F&& f) {
   } catch (const std::bad_alloc&) {
     g_last_error = "host allocation failed";
     return ALSNCG_ENOMEM;
+  } catch (const alsncg::DuplicateRatingError& e) {
+    g_last_error = e.what();
+    return ALSNCG_EDUP;
+  } catch (const alsncg::DataError& e) {
+    g_last_error = e.what();
+    return ALSNCG_EDATA;
+  } catch (const std::logic_error& e) {
+    if (dynamic_cast<const std::invalid_argument*>(&e) == nullptr &&
+        dynamic_cast<const std::out_of_range*>(&e) == nullptr) {
+      g_last_error = e.what();
+      return ALSNCG_ELOGIC;
+    }
+    g_last_error = e.what();
+    return ALSNCG_EINVAL;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return ALSNCG_EINVAL;
@@ -191,6 +207,63 @@ int alsncg_ctx_create_dist(int device, int rank, int world, const unsigned char 
       std::memcpy(&u, id, 128);
       AB2_NCCL(ab2::nccl().CommInitRank(&c->impl->comm, world, u, rank));
     }
+    *out = c.release();
+  });
+}
+
+int alsncg_write_trace_csv(const char* path, const alsncg_trace_record* recs, int n) {
+  return guarded([&] {
+    need(path && (recs || n == 0) && n >= 0, "null argument");
+    alsncg::ConvergenceTrace t;
+    for (int i = 0; i < n; ++i) {
+      alsncg::TraceRecord r;
+      r.iter = recs[i].iter;
+      r.loss = recs[i].loss;
+      r.grad_norm = recs[i].grad_norm;
+      r.elapsed_seconds = recs[i].elapsed_seconds;
+      r.backtracks = recs[i].backtracks;
+      r.shuffled_columns = recs[i].shuffled_columns;
+      r.restarted = recs[i].restarted != 0;
+      t.records.push_back(r);
+    }
+    alsncg::harness::write_trace_csv(path, t);
+  });
+}
+
+int alsncg_read_trace_csv(const char* path, alsncg_trace_record* recs, int cap, int* n) {
+  return guarded([&] {
+    need(path && n && (recs || cap == 0), "null argument");
+    const alsncg::ConvergenceTrace t = alsncg::harness::read_trace_csv(path);
+    *n = static_cast<int>(t.records.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+      const alsncg::TraceRecord& r = t.records[i];
+      recs[i] = {r.iter, r.loss, r.grad_norm, r.elapsed_seconds, r.backtracks, r.shuffled_columns,
+                 r.restarted ? 1 : 0};
+    }
+  });
+}
+
+int alsncg_loopgroup_create(int world, alsncg_loopgroup** out) {
+  return guarded([&] {
+    need(out && world >= 1, "bad world");
+    *out = reinterpret_cast<alsncg_loopgroup*>(new ab2::LoopGroup(world));
+  });
+}
+
+int alsncg_loopgroup_destroy(alsncg_loopgroup* g) {
+  return guarded([&] { delete reinterpret_cast<ab2::LoopGroup*>(g); });
+}
+
+int alsncg_ctx_create_loopback(int device, int rank, alsncg_loopgroup* group, alsncg_ctx** out) {
+  return guarded([&] {
+    auto* G = reinterpret_cast<ab2::LoopGroup*>(group);
+    need(out && G && rank >= 0 && rank < G->world, "bad rank/group");
+    auto c = std::make_unique<alsncg_ctx>();
+    c->impl = std::make_unique<ab2::Ctx>(device);
+    c->impl->rank = rank;
+    c->impl->world = G->world;
+    c->impl->loop = G;
+    G->ranks[rank] = c->impl.get();
     *out = c.release();
   });
 }
@@ -375,9 +448,7 @@ int alsncg_half_sweep(alsncg_ratings* r, int kind, int n_f, const double* src, d
       ab2::allgather_rows(ctx, d, mb, ld);
       unstage_rows(R, n_f, d + item_off, R.n_m, out);
     }
-    unsigned fb = 0;
-    AB2_CUDA(cudaMemcpy(&fb, ctx->d_counters + 17, sizeof fb, cudaMemcpyDeviceToHost));
-    if (fallback_columns) *fallback_columns = static_cast<int>(fb);
+    if (fallback_columns) *fallback_columns = static_cast<int>(ctx->counter_total(17));
   });
 }
 
@@ -398,9 +469,7 @@ int alsncg_als_sweep(alsncg_ratings* r, int n_f, const double* x, double lambda,
     ab2::launch_half_sweep(R, 1, n_f, d, lambda, d, 17);
     gather_flat(R, n_f, d);
     unstage_rows(R, n_f, d, static_cast<int64_t>(R.n_u) + R.n_m, out);
-    unsigned fb = 0;
-    AB2_CUDA(cudaMemcpy(&fb, ctx->d_counters + 17, sizeof fb, cudaMemcpyDeviceToHost));
-    if (fallback_columns) *fallback_columns = static_cast<int>(fb);
+    if (fallback_columns) *fallback_columns = static_cast<int>(ctx->counter_total(17));
   });
 }
 
@@ -458,12 +527,7 @@ int alsncg_dev_half_sweep(alsncg_ratings* r, int kind, int n_f, const double* d_
       for (int& b : mb) b += R.n_u;
       ab2::allgather_rows(ctx, d_out, mb, ld);
     }
-    if (fallback_columns) {
-      unsigned fb = 0;
-      AB2_CUDA(cudaMemcpyAsync(&fb, ctx->d_counters + 17, sizeof fb, cudaMemcpyDeviceToHost, ctx->stream));
-      ctx->sync();
-      *fallback_columns = static_cast<int>(fb);
-    }
+    if (fallback_columns) *fallback_columns = static_cast<int>(ctx->counter_total(17));
   });
 }
 

@@ -5,6 +5,8 @@
 // process-wide default context (device ALSNCG_DEVICE, default 0).
 #include <algorithm>
 #include <atomic>
+#include <charconv>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -19,6 +21,7 @@
 #include "alsncg/als.hpp"
 #include "alsncg/config.hpp"
 #include "alsncg/factors.hpp"
+#include "alsncg/harness.hpp"
 #include "alsncg/linesearch.hpp"
 #include "alsncg/ncg.hpp"
 #include "alsncg/parallel.hpp"
@@ -340,6 +343,82 @@ LoadedModel load_model(const std::string& path) {
   if (!in) throw DataError(path + ": truncated snapshot");
   return l;
 }
+
+// ----------------------------------------------------------- trace CSV --
+// harness.cpp:80-127 (file format and error behaviour of the reference).
+namespace harness {
+namespace {
+
+std::string fmt17(double v) {
+  char b[40];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+
+template <typename T>
+T parse_field(const std::string& f, const std::string& path, const char* what) {
+  T v{};
+  const auto r = std::from_chars(f.data(), f.data() + f.size(), v);
+  if (r.ec != std::errc() || r.ptr != f.data() + f.size())
+    throw DataError(path + ": bad " + what + " field '" + f + "'");
+  return v;
+}
+
+}  // namespace
+
+void write_trace_csv(const std::string& path, const ConvergenceTrace& trace) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw DataError("cannot write " + path);
+  out << "iter,loss,grad_norm,elapsed_s,backtracks,shuffled_columns\n";
+  for (const TraceRecord& t : trace.records)
+    out << t.iter << ',' << fmt17(t.loss) << ',' << fmt17(t.grad_norm) << ',' << fmt17(t.elapsed_seconds)
+        << ',' << t.backtracks << ',' << t.shuffled_columns << '\n';
+  if (!out) throw DataError("failed writing " + path);
+}
+
+ConvergenceTrace read_trace_csv(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataError("cannot open " + path);
+  ConvergenceTrace trace;
+  std::string line;
+  bool header = true;
+  while (std::getline(in, line)) {
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    if (line.empty()) continue;
+    if (header) {
+      header = false;
+      continue;
+    }
+    std::vector<std::string> f;
+    for (size_t b = 0;;) {
+      const size_t c = line.find(',', b);
+      f.push_back(line.substr(b, c == std::string::npos ? std::string::npos : c - b));
+      if (c == std::string::npos) break;
+      b = c + 1;
+    }
+    if (f.size() != 6) throw DataError(path + ": expected 6 trace columns");
+    TraceRecord t;
+    t.iter = static_cast<int>(parse_field<std::int64_t>(f[0], path, "integer"));
+    t.loss = parse_field<double>(f[1], path, "numeric");
+    t.grad_norm = parse_field<double>(f[2], path, "numeric");
+    t.elapsed_seconds = parse_field<double>(f[3], path, "numeric");
+    t.backtracks = static_cast<int>(parse_field<std::int64_t>(f[4], path, "integer"));
+    t.shuffled_columns = parse_field<std::int64_t>(f[5], path, "integer");
+    trace.append(t);
+  }
+  if (trace.empty()) throw DataError(path + ": empty trace");
+  return trace;
+}
+
+double mean_iteration_seconds(const ConvergenceTrace& trace) {
+  if (trace.empty()) throw DataError("mean_iteration_seconds: empty trace");
+  const TraceRecord& a = trace.records.front();
+  const TraceRecord& b = trace.records.back();
+  if (a.iter == b.iter) return 0.0;
+  return (b.elapsed_seconds - a.elapsed_seconds) / static_cast<double>(b.iter - a.iter);
+}
+
+}  // namespace harness
 
 // ------------------------------------------------------------- drivers --
 namespace {

@@ -85,6 +85,7 @@ void* Ctx::scratch(int slot, size_t bytes) {
 
 int Ctx::begin_launch(const char* name) {
   ++launches;
+  launch_name = name;
   if (!profiling) return -1;
   int k = 0;
   for (; k < static_cast<int>(stats.size()); ++k)
@@ -111,7 +112,9 @@ int Ctx::begin_launch(const char* name) {
 
 void Ctx::end_launch(int token) {
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw Error(ALSNCG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    throw Error(ALSNCG_ECUDA, std::string("kernel launch (") + (launch_name ? launch_name : "?") +
+                                  "): " + cudaGetErrorString(e));
   if (token >= 0) AB2_CUDA(cudaEventRecord(pending[token].b, stream));
 }
 
@@ -130,21 +133,46 @@ void Ctx::collect_stats() {
 
 void Ctx::sync() { AB2_CUDA(cudaStreamSynchronize(stream)); }
 
+unsigned Ctx::counter_total(int slot) {
+  unsigned* d = d_counters + slot;
+  if (world > 1) {
+    allreduce_sum_u32(this, d, d_counters + 24, 1);
+    d = d_counters + 24;
+  }
+  unsigned h = 0;
+  AB2_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, stream));
+  sync();
+  return h;
+}
+
+int Ctx::prepare_kernel(const void* fn, int smem_limit, int threads, size_t smem) {
+  auto it = kernel_attr.find(fn);
+  if (it != kernel_attr.end()) return it->second;
+  AB2_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_limit));
+  int per_sm = 0;
+  if (threads > 0) AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  per_sm = std::max(per_sm, 1);
+  kernel_attr.emplace(fn, per_sm);
+  return per_sm;
+}
+
 void Ctx::fetch_scalars(int n) {
   AB2_CUDA(cudaMemcpyAsync(h_scalars, d_scalars, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
   AB2_CUDA(cudaStreamSynchronize(stream));
 }
 
 L2Window::L2Window(Ctx* c, const void* base, size_t bytes) : ctx(c) {
-  static int max_persist = -1, max_window = 0;
-  if (max_persist < 0) {
-    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device) != cudaSuccess)
-      max_persist = 0;
-    if (cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device) != cudaSuccess)
-      max_window = 0;
-    if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
+  // per-context (= per-device) limits, queried once per context
+  if (c->l2_max_persist < 0) {
+    int mp = 0, mw = 0;
+    if (cudaDeviceGetAttribute(&mp, cudaDevAttrMaxPersistingL2CacheSize, c->device) != cudaSuccess) mp = 0;
+    if (cudaDeviceGetAttribute(&mw, cudaDevAttrMaxAccessPolicyWindowSize, c->device) != cudaSuccess) mw = 0;
+    if (mp > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(mp));
     cudaGetLastError();
+    c->l2_max_window = mw;
+    c->l2_max_persist = mp;
   }
+  const int max_persist = c->l2_max_persist, max_window = c->l2_max_window;
   if (max_persist <= 0 || max_window <= 0 || bytes == 0) return;
   cudaStreamAttrValue v = {};
   v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
@@ -180,8 +208,72 @@ std::vector<int> partition_rows(int n_rows, const int64_t* ptr, int world, int a
   return b;
 }
 
+LoopGroup::LoopGroup(int w) : world(w), ranks(w, nullptr), slot(w, nullptr) {}
+
+void LoopGroup::barrier() {
+  std::unique_lock<std::mutex> lk(m_);
+  const unsigned g = gen_;
+  if (++arrived_ == world) {
+    arrived_ = 0;
+    ++gen_;
+    cv_.notify_all();
+  } else {
+    cv_.wait(lk, [&] { return gen_ != g; });
+  }
+}
+
+namespace {
+// Loopback collective skeleton: publish this rank's buffer, drain every
+// stream, run `body` (reads peers' published buffers), drain, release.
+template <typename F>
+void loop_collective(Ctx* ctx, void* buf, F&& body) {
+  LoopGroup& G = *ctx->loop;
+  G.slot[ctx->rank] = buf;
+  ctx->sync();
+  G.barrier();
+  body(G);
+  ctx->sync();
+  G.barrier();
+}
+
+template <typename T>
+void loop_allreduce(Ctx* ctx, const T* send, T* recv, int n) {
+  loop_collective(ctx, const_cast<T*>(send), [&](LoopGroup& G) {
+    std::vector<T> acc(n, 0), h(n);
+    for (int r = 0; r < G.world; ++r) {  // rank order
+      AB2_CUDA(cudaMemcpy(h.data(), G.slot[r], sizeof(T) * n, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) acc[i] += h[i];
+    }
+    G.barrier();  // every rank has read every send buffer (send may alias recv)
+    AB2_CUDA(cudaMemcpy(recv, acc.data(), sizeof(T) * n, cudaMemcpyHostToDevice));
+  });
+}
+}  // namespace
+
+void allreduce_sum_u32(Ctx* ctx, const unsigned* send, unsigned* recv, int n) {
+  if (ctx->loop) return loop_allreduce(ctx, send, recv, n);
+  AB2_NCCL(nccl().AllReduce(send, recv, n, ncclUint32, ncclSum, ctx->comm, ctx->stream));
+}
+
+void allreduce_sum_u64(Ctx* ctx, const unsigned long long* send, unsigned long long* recv, int n) {
+  if (ctx->loop) return loop_allreduce(ctx, send, recv, n);
+  AB2_NCCL(nccl().AllReduce(send, recv, n, ncclUint64, ncclSum, ctx->comm, ctx->stream));
+}
+
 void allgather_rows(Ctx* ctx, double* rows, const std::vector<int>& bounds, int ld) {
   if (ctx->world <= 1) return;
+  if (ctx->loop) {  // every peer's rows [bounds[r], bounds[r+1]) into this rank's buffer
+    loop_collective(ctx, rows, [&](LoopGroup& G) {
+      for (int r = 0; r < G.world; ++r) {
+        const size_t count = static_cast<size_t>(bounds[r + 1] - bounds[r]) * ld;
+        if (r == ctx->rank || count == 0) continue;
+        const size_t off = static_cast<size_t>(bounds[r]) * ld;
+        AB2_CUDA(cudaMemcpyAsync(rows + off, static_cast<double*>(G.slot[r]) + off, sizeof(double) * count,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    });
+    return;
+  }
   AB2_NCCL(nccl().GroupStart());
   for (int r = 0; r < ctx->world; ++r) {
     const size_t count = static_cast<size_t>(bounds[r + 1] - bounds[r]) * ld;
@@ -311,8 +403,10 @@ const SegPlan& DevRatings::plan(int kind, int S) {
   P->m_row = P->seg_slot + ns;
   P->m_slot0 = P->m_row + nm;
   P->m_nslot = P->m_slot0 + nm;
+  // stream-ordered with the kernels that read the plan (ctx->stream is a
+  // non-blocking stream, so a legacy-stream cudaMemcpy would not order them)
   auto up = [&](void* d, const void* h, size_t n) {
-    if (n) AB2_CUDA(cudaMemcpy(d, h, n, cudaMemcpyHostToDevice));
+    if (n) AB2_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, ctx->stream));
   };
   up(P->seg_beg, beg.data(), beg.size() * 8);
   up(P->seg_row, row.data(), row.size() * 4);
@@ -321,6 +415,7 @@ const SegPlan& DevRatings::plan(int kind, int S) {
   up(P->m_row, mrow.data(), mrow.size() * 4);
   up(P->m_slot0, mslot0.data(), mslot0.size() * 4);
   up(P->m_nslot, mnslot.data(), mnslot.size() * 4);
+  ctx->sync();  // the host vectors go out of scope
   const SegPlan& ref = *P;
   m.emplace(S, std::move(P));
   return ref;
@@ -397,8 +492,10 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
   P->row_slot0 = P->seg_slot + ns;
   P->row_nslot = P->row_slot0 + nr;
   P->multi_rows = P->row_nslot + nr;
+  // stream-ordered with the kernels that read the plan (ctx->stream is a
+  // non-blocking stream, so a legacy-stream cudaMemcpy would not order them)
   auto up = [&](void* d, const void* h, size_t n) {
-    if (n) AB2_CUDA(cudaMemcpy(d, h, n, cudaMemcpyHostToDevice));
+    if (n) AB2_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, ctx->stream));
   };
   up(P->seg_beg, sbeg.data(), sbeg.size() * 8);
   up(P->seg_row, srow.data(), srow.size() * 4);
@@ -407,6 +504,7 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
   up(P->row_slot0, row_slot0.data(), static_cast<size_t>(v.nrows) * 4);
   up(P->row_nslot, row_nslot.data(), static_cast<size_t>(v.nrows) * 4);
   up(P->multi_rows, multi.data(), multi.size() * 4);
+  ctx->sync();  // the host vectors go out of scope
   const HsPlan& ref = *P;
   m.emplace(key, std::move(P));
   return ref;
@@ -417,8 +515,7 @@ std::pair<int64_t, int64_t> DevRatings::routing_totals(int n_blocks) {
   if (it != routing.end()) return it->second;
   unsigned long long* d = static_cast<unsigned long long*>(ctx->scratch(5, 16));
   launch_routing_count(*this, n_blocks, d);
-  if (ctx->world > 1)
-    AB2_NCCL(nccl().AllReduce(d, d, 2, ncclUint64, ncclSum, ctx->comm, ctx->stream));
+  if (ctx->world > 1) allreduce_sum_u64(ctx, d, d, 2);
   unsigned long long h[2];
   AB2_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();

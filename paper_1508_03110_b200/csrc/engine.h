@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <mutex>
 #include <functional>
 #include <map>
 #include <memory>
@@ -51,6 +53,28 @@ constexpr int kMaxGramBlocks = 26;  // n_f <= 206
 constexpr int kMaxRank = 206;
 
 // -------------------------------------------------------------- context --
+struct Ctx;
+
+// In-process stand-in for an NCCL communicator (tests only): `world` contexts
+// in one process, each driven by its own host thread, exchange through
+// device-to-device copies between their buffers.  Every collective is
+// barrier -> every rank's stream drained -> barrier -> copies -> barrier, so
+// no rank touches a buffer a peer still reads.  It exercises exactly the
+// sharded code paths (partition_rows, per-shard kernels, ragged row
+// exchange, rank-ordered tile sums) with the GPU work serialised.
+struct LoopGroup {
+  explicit LoopGroup(int w);
+  int world;
+  std::vector<Ctx*> ranks;  // registered by the contexts
+  std::vector<void*> slot;  // per-rank buffer pointer of the current collective
+  void barrier();
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  unsigned gen_ = 0;
+};
+
 struct KernelStat {
   std::string name;
   int64_t launches = 0;
@@ -72,8 +96,10 @@ struct Ctx {
   std::function<void()> side_work;
   bool side_join = false;
   ncclComm_t comm = nullptr;
+  LoopGroup* loop = nullptr;  // in-process communicator (tests), instead of comm
   bool profiling = false;
   int64_t launches = 0;
+  const char* launch_name = nullptr;  // last begin_launch (error messages)
   std::vector<KernelStat> stats;
   struct Pending {
     int stat;
@@ -89,6 +115,13 @@ struct Ctx {
   double* d_scalars = nullptr;  // small result slots
   double* h_scalars = nullptr;  // pinned mirror
   int sm_count = 148;
+  // per-device caches (one Ctx per device): L2 persistence limits and the
+  // set of kernels whose dynamic shared-memory limit was raised on this device
+  int l2_max_persist = -1, l2_max_window = 0;
+  std::map<const void*, int> kernel_attr;  // kernel -> occupancy (CTAs per SM) after the attribute was set
+  // Raises `fn`'s dynamic shared-memory limit on this context's device once
+  // and returns its occupancy (CTAs per SM) at `threads`/`smem` (>= 1).
+  int prepare_kernel(const void* fn, int smem_limit, int threads, size_t smem);
 
   explicit Ctx(int dev);
   ~Ctx();
@@ -104,6 +137,9 @@ struct Ctx {
   void collect_stats();  // syncs and folds pending events into stats
   void sync();
   void fetch_scalars(int n);  // d_scalars[0..n) -> h_scalars (synchronous)
+  // d_counters[slot] summed over the ranks (NCCL all-reduce when world > 1;
+  // uses counter slot 24 as the receive buffer), read back synchronously.
+  unsigned counter_total(int slot);
 };
 
 // -------------------------------------------------------- device ratings --
@@ -243,5 +279,9 @@ void launch_unpad_rows(Ctx* ctx, int64_t rows, int n_f, const double* padded, do
 // Multi-GPU: replicate row ranges [b[r], b[r+1]) of a row-major buffer from
 // their owning rank to all ranks (grouped in-place broadcasts over NCCL).
 void allgather_rows(Ctx* ctx, double* rows, const std::vector<int>& bounds, int ld);
+// In-place sum over the ranks of n unsigned 32/64-bit counters (NCCL
+// all-reduce, or the loopback group).
+void allreduce_sum_u32(Ctx* ctx, const unsigned* send, unsigned* recv, int n);
+void allreduce_sum_u64(Ctx* ctx, const unsigned long long* send, unsigned long long* recv, int n);
 
 }  // namespace ab2

@@ -12,7 +12,7 @@ namespace {
 // ------------------------------------------------------------ fallback --
 // Least-norm solve for listed rows.  Workspace per CTA: W (n x n), Q (n x n).
 constexpr int kFbThreads = 256;
-constexpr int kFbBlocks = 32;
+constexpr int kFbBlocks = 296;  // 2 per SM: rank-deficient columns (lambda*n = 0) are solved in parallel
 
 __device__ void fb_block_sum2(double& a, double& b, double* sh) {
   for (int off = 16; off > 0; off >>= 1) {

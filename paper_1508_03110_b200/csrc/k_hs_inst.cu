@@ -1167,12 +1167,8 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     a.m_nslot = P.m_nslot;
     a.n_multi = P.n_multi;
     const size_t smem = sizeof(double) * hs_group_doubles<NB, GW>(a.ld) * C::GPC;
-    static bool attr_set = false;
-    if (!attr_set) {
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_main<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_reduce<NB, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr_set = true;
-    }
+    ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_main<NB, GW>), 227 * 1024, 0, 0);
+    ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_reduce<NB, GW>), 227 * 1024, 0, 0);
     if (P.n_slots > 0)
       a.partial = static_cast<double*>(ctx->scratch(2, sizeof(double) * C::PART * P.n_slots));
     {
@@ -1194,16 +1190,15 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
     using GC = HsCfg<NB, GS::W>;
     const size_t gsmem = sizeof(double) * std::max<size_t>(2 * kGramStage * GC::LDS + 2,
                                                            size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
-    static bool attr_set = false;
-    if (!attr_set) {
-      if constexpr (kGramWs<NB>)
-        AB2_CUDA(cudaFuncSetAttribute(k_hs_gram_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      else
-        AB2_CUDA(cudaFuncSetAttribute(k_hs_gram<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      AB2_CUDA(cudaFuncSetAttribute(k_hs_solve_ws<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    WsSolve<NB>::TEAMS * WsSolve<NB>::TEAM_BYTES));
-      attr_set = true;
-    }
+    // per-device attribute / occupancy cache (Ctx::prepare_kernel)
+    int gram_per_sm = 1;
+    if constexpr (kGramWs<NB>)
+      gram_per_sm = ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_gram_ws<NB>), 227 * 1024,
+                                        (WsShape<NB>::GR + 1) * 32, WsShape<NB>::smem_bytes());
+    else
+      ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_gram<NB>), 227 * 1024, 0, 0);
+    ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_solve_ws<NB>),
+                        WsSolve<NB>::TEAMS * WsSolve<NB>::TEAM_BYTES, 0, 0);
     double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
     // Keep the gathered source factor rows resident in L2 while the Gram
     // stream (written with evict-first stores) passes through.
@@ -1218,13 +1213,7 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
         if (b.seg1 > b.seg0) {
           using WS = WsShape<NB>;
           const int nseg = b.seg1 - b.seg0;
-          static int per_sm = 0;
-          if (per_sm == 0) {
-            AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hs_gram_ws<NB>, (WS::GR + 1) * 32,
-                                                                   WS::smem_bytes()));
-            per_sm = std::max(per_sm, 1);
-          }
-          const int grid = std::min(nseg, per_sm * ctx->sm_count);  // persistent CTAs
+          const int grid = std::min(nseg, gram_per_sm * ctx->sm_count);  // persistent CTAs
           int* next_seg = static_cast<int*>(ctx->scratch(8, sizeof(int)));
           AB2_CUDA(cudaMemsetAsync(next_seg, 0, sizeof(int), ctx->stream));
           const int tok = ctx->begin_launch("halfsweep_gram");

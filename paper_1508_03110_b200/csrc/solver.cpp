@@ -192,11 +192,7 @@ void Solver::model(double* host_packed) {
 }
 
 int Solver::fallback_columns() {
-  unsigned h = 0;
-  AB2_CUDA(cudaMemcpyAsync(&h, ctx_->d_counters + kCounterFallback, sizeof h, cudaMemcpyDeviceToHost,
-                           ctx_->stream));
-  ctx_->sync();
-  return static_cast<int>(h);
+  return static_cast<int>(ctx_->counter_total(kCounterFallback));  // summed over the ranks
 }
 
 void Solver::record(int backtracks, bool restarted) {

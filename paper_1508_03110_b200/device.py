@@ -22,6 +22,18 @@ class Context:
         self.handle = h
         self.device, self.rank, self.world = device, rank, world
 
+    @classmethod
+    def loopback(cls, device, rank, group):
+        """Rank `rank` of an in-process LoopGroup (testing aid: the sharded
+        path on one GPU, one host thread per rank)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        check(lib().alsncg_ctx_create_loopback(device, rank, group.handle, C.byref(h)))
+        self.handle = h
+        self.device, self.rank, self.world = device, rank, group.world
+        self._group = group  # keep the group alive as long as its ranks
+        return self
+
     @staticmethod
     def nccl_unique_id():
         buf = (C.c_ubyte * 128)()
@@ -62,6 +74,23 @@ class Context:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class LoopGroup:
+    """alsncg_loopgroup: in-process stand-in for an NCCL communicator (tests)."""
+
+    def __init__(self, world):
+        h = C.c_void_p()
+        check(lib().alsncg_loopgroup_create(world, C.byref(h)))
+        self.handle, self.world = h, world
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().alsncg_loopgroup_destroy(self.handle)
+                self.handle = None
         except Exception:
             pass
 
