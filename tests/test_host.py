@@ -153,3 +153,47 @@ def test_synth_generator_contract():
     assert again.uidx.tobytes() == R.uidx.tobytes() and again.uval.tobytes() == R.uval.tobytes()
     u, i, val = P.synth.generate_triples(300, 200, 300 * 20 + 4567, 7)
     assert len(u) == 300 * 20 + 4567 and np.bincount(u).min() >= 20
+
+
+def _big_triples(seed, n_u=40_000, n_m=3_000, nnz=1_500_000):
+    """A ~1.5M-rating instance (multi-threaded CSR build), shuffled input order."""
+    rng = np.random.default_rng(seed)
+    key = rng.choice(n_u * n_m, size=nnz, replace=False)
+    rng.shuffle(key)
+    users = (key // n_m).astype(np.int32)
+    items = (key % n_m).astype(np.int32)
+    values = np.round(rng.uniform(0.5, 5.0, nnz) * 2) / 2
+    return n_u, n_m, users, items, values
+
+
+def test_csr_threaded_build_bit_exact_and_errors_vs_oracle():
+    n_u, n_m, u, i, v = _big_triples(5)
+    R = P.RatingsMatrix.from_triples(n_u, n_m, users=u, items=i, values=v)
+    O = OracleRatings(n_u, n_m, u, i, v)
+    _csr_equal(R, O)
+    # the first bad triple in INPUT order is the one reported
+    u2, v2 = u.copy(), v.copy()
+    u2[900_000] = n_u + 5
+    v2[300_000] = np.nan
+    with pytest.raises(P.DataError, match="non-finite"):
+        P.RatingsMatrix.from_triples(n_u, n_m, users=u2, items=i, values=v2)
+    with pytest.raises(P.DataError, match=f"user {n_u + 5}"):
+        P.RatingsMatrix.from_triples(n_u, n_m, users=u2, items=i, values=v)
+    # duplicates: the first one in (user, item) order is reported (ratings.cpp:47-51)
+    u3, i3 = u.copy(), i.copy()
+    for a, b in ((1_200_000, 10), (50, 700_000)):
+        u3[a], i3[a] = u3[b], i3[b]
+    first = min((int(u3[b]), int(i3[b])) for b in (10, 700_000))
+    with pytest.raises(P.DuplicateRatingError, match=f"user {first[0]}, item {first[1]}"):
+        P.RatingsMatrix.from_triples(n_u, n_m, users=u3, items=i3, values=v)
+
+
+def test_threaded_generator_bitwise_vs_sequential_oracle():
+    # odd truth-normal count (spare carried into the rating noise) and a
+    # multi-chunk stream: 97 users x 61 items, then 50k users
+    from oracle.pyoracle import synth_triples
+    for (n_u, n_m, nnz, seed) in ((97, 61, 2_100, 7), (50_001, 2_001, 3_000_000, 11)):
+        a = synth_triples(n_u, n_m, nnz, seed)
+        b = P.synth.generate_triples(n_u, n_m, nnz, seed)
+        for x, y in zip(a, b):
+            assert x.tobytes() == y.tobytes()
