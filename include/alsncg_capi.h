@@ -133,6 +133,16 @@ int alsncg_ctx_create(int device, alsncg_ctx** out);
 int alsncg_nccl_unique_id(unsigned char id[128]);
 int alsncg_ctx_create_dist(int device, int rank, int world, const unsigned char id[128],
                            alsncg_ctx** out);
+/* ranking::mean_ranking_accuracy (ranking.cpp:90-109): mean over users of the
+ * top-t Kendall-tau accuracy of model_k's item ranking against the final
+ * model's (FactorModel layout: n_f doubles per user / item column).  Scores
+ * use the reference's exact arithmetic, so ties and orders are the
+ * reference's; the per-user values are summed in user order on the host.
+ * ALSNCG_EINVAL for t outside [1, n_m] or no users. */
+int alsncg_mean_ranking_accuracy(alsncg_ctx* ctx, int n_f, int n_u, int n_m, const double* user_k,
+                                 const double* item_k, const double* user_final, const double* item_final,
+                                 int t, double* out);
+
 /* Trace CSV of one run (harness.cpp:80-118: header
  * "iter,loss,grad_norm,elapsed_s,backtracks,shuffled_columns", %.17g doubles;
  * the restarted flag is not part of the file).  read returns the record count

@@ -415,3 +415,13 @@ def beta_bar(gn, gp, bn, bp):
     e = np.zeros(1)
     return port().orc_beta_bar(arrs[0].size, 0, _nonempty(arrs[0]), e, _nonempty(arrs[1]), e,
                                _nonempty(arrs[2]), e, _nonempty(arrs[3]), e)
+
+
+def ref_mean_ranking_accuracy(n_f, n_u, n_m, user_k, item_k, user_f, item_f, t, n_workers=1):
+    """The reference's ranking::mean_ranking_accuracy (oracle/_ref)."""
+    L = ref()
+    L.ref_mean_ranking_accuracy.restype = C.c_double
+    L.ref_mean_ranking_accuracy.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_int,
+                                            C.c_int]
+    a = [np.ascontiguousarray(x, dtype=np.float64) for x in (user_k, item_k, user_f, item_f)]
+    return L.ref_mean_ranking_accuracy(n_f, n_u, n_m, *a, t, n_workers)

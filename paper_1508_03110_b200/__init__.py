@@ -5,7 +5,7 @@ vector work) as sm_100a CUDA kernels behind the reference's solver API.
 Python mirror of /root/reference/proj/include/alsncg (module per header);
 every compute call goes through the C-ABI in include/alsncg_capi.h.
 """
-from . import als, config, factors, harness, linesearch, ncg, ratings  # noqa: F401
+from . import als, config, factors, harness, linesearch, ncg, ranking, ratings  # noqa: F401
 from ._lib import LIB_PATH, AlsncgError, lib  # noqa: F401
 from .config import ConvergenceTrace, QuarticPoly, SolveResult, SolverConfig, TraceRecord  # noqa: F401
 from .device import Context, DeviceBuffer, LoopGroup, default_context, row_stride  # noqa: F401

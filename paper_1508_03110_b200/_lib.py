@@ -58,6 +58,7 @@ SIGNATURES = {
     "alsncg_ctx_create_dist": (i32, [i32, i32, i32, vp, C.POINTER(vp)]),
     "alsncg_loopgroup_create": (i32, [i32, C.POINTER(vp)]),
     "alsncg_write_trace_csv": (i32, [C.c_char_p, vp, i32]),
+    "alsncg_mean_ranking_accuracy": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, i32, dp]),
     "alsncg_read_trace_csv": (i32, [C.c_char_p, vp, i32, ip]),
     "alsncg_loopgroup_destroy": (i32, [vp]),
     "alsncg_ctx_create_loopback": (i32, [i32, i32, vp, C.POINTER(vp)]),

@@ -2,6 +2,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -208,6 +209,34 @@ int alsncg_ctx_create_dist(int device, int rank, int world, const unsigned char 
       AB2_NCCL(ab2::nccl().CommInitRank(&c->impl->comm, world, u, rank));
     }
     *out = c.release();
+  });
+}
+
+int alsncg_mean_ranking_accuracy(alsncg_ctx* ctx, int n_f, int n_u, int n_m, const double* user_k,
+                                 const double* item_k, const double* user_final, const double* item_final,
+                                 int t, double* out) {
+  return guarded([&] {
+    need(ctx && out && n_f >= 1 && n_u >= 0 && n_m >= 0, "mean_ranking_accuracy: bad arguments");
+    if (n_u == 0) throw std::invalid_argument("mean_ranking_accuracy: no users");  // ranking.cpp:95
+    if (t < 1 || t > n_m) throw std::invalid_argument("ranking_accuracy: t out of range");  // ranking.cpp:63
+    need(user_k && item_k && user_final && item_final, "null argument");
+    ab2::Ctx* c = ctx->impl.get();
+    AB2_CUDA(cudaSetDevice(c->device));
+    const size_t nu = static_cast<size_t>(n_f) * n_u, nm = static_cast<size_t>(n_f) * n_m;
+    double* d = static_cast<double*>(c->alloc(sizeof(double) * (2 * nu + 2 * nm + n_u)));
+    AB2_CUDA(cudaMemcpyAsync(d, user_k, sizeof(double) * nu, cudaMemcpyHostToDevice, c->stream));
+    AB2_CUDA(cudaMemcpyAsync(d + nu, item_k, sizeof(double) * nm, cudaMemcpyHostToDevice, c->stream));
+    AB2_CUDA(cudaMemcpyAsync(d + nu + nm, user_final, sizeof(double) * nu, cudaMemcpyHostToDevice, c->stream));
+    AB2_CUDA(cudaMemcpyAsync(d + 2 * nu + nm, item_final, sizeof(double) * nm, cudaMemcpyHostToDevice, c->stream));
+    double* dq = d + 2 * nu + 2 * nm;
+    ab2::launch_mean_ranking(c, n_f, n_u, n_m, d, d + nu, d + nu + nm, d + 2 * nu + nm, t, dq);
+    std::vector<double> q(n_u);
+    AB2_CUDA(cudaMemcpyAsync(q.data(), dq, sizeof(double) * n_u, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    c->release(d);
+    double sum = 0.0;  // ranking.cpp:104-107: sequential in user order
+    for (double v : q) sum += v;
+    *out = sum / static_cast<double>(n_u);
   });
 }
 

@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <numbers>
+#include <numeric>
 #include <stdexcept>
 #include <thread>
 
@@ -25,6 +26,7 @@
 #include "alsncg/linesearch.hpp"
 #include "alsncg/ncg.hpp"
 #include "alsncg/parallel.hpp"
+#include "alsncg/ranking.hpp"
 #include "alsncg/ratings.hpp"
 #include "alsncg/rng.hpp"
 #include "alsncg/snapshot.hpp"
@@ -343,6 +345,66 @@ LoadedModel load_model(const std::string& path) {
   if (!in) throw DataError(path + ": truncated snapshot");
   return l;
 }
+
+// ------------------------------------------------------------- ranking --
+namespace ranking {
+
+RankingVector rank_items(const FactorModel& model, int user) {
+  if (user < 0 || user >= model.n_u) throw std::out_of_range("rank_items: user index");
+  const double* u = model.user_col(user);
+  std::vector<double> sc(static_cast<size_t>(model.n_m));
+  for (int j = 0; j < model.n_m; ++j) {
+    const double* m = model.item_col(j);
+    double d = 0.0;
+    for (int k = 0; k < model.n_f; ++k) d += u[k] * m[k];  // sequential, no FMA (-ffp-contract=off)
+    sc[j] = d;
+  }
+  RankingVector order(static_cast<size_t>(model.n_m));
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return sc[a] != sc[b] ? sc[a] > sc[b] : a < b; });
+  return order;
+}
+
+double ranking_accuracy(const RankingVector& p1, const RankingVector& p2, int t) {
+  const int n = static_cast<int>(p1.size());
+  auto is_perm = [n](const RankingVector& p) {
+    if (static_cast<int>(p.size()) != n) throw std::invalid_argument("ranking_accuracy: size mismatch");
+    std::vector<char> seen(static_cast<size_t>(n), 0);
+    for (int v : p) {
+      if (v < 0 || v >= n || seen[v]) throw std::invalid_argument("ranking_accuracy: not a permutation");
+      seen[v] = 1;
+    }
+  };
+  is_perm(p1);
+  is_perm(p2);
+  if (t < 1 || t > n) throw std::invalid_argument("ranking_accuracy: t out of range");
+  // closed form of the swap walk: rank2(p1[r]) minus the earlier picks that
+  // p2 ranks ahead of it (the same count the reference's working-copy walk makes)
+  std::vector<int> pos(static_cast<size_t>(n));
+  for (int r = 0; r < n; ++r) pos[p2[r]] = r;
+  std::int64_t swaps = 0;
+  for (int r = 0; r < t; ++r) {
+    int ahead = 0;
+    for (int q = 0; q < r; ++q) ahead += pos[p1[q]] < pos[p1[r]] ? 1 : 0;
+    swaps += pos[p1[r]] - ahead;
+  }
+  const std::int64_t smax = static_cast<std::int64_t>(t) * (2 * static_cast<std::int64_t>(n) - t - 1) / 2;
+  if (smax == 0) return 1.0;
+  return 1.0 - static_cast<double>(swaps) / static_cast<double>(smax);
+}
+
+double mean_ranking_accuracy(const FactorModel& model_at_k, const FactorModel& model_final, int t, int n_workers) {
+  (void)n_workers;
+  if (model_at_k.n_f != model_final.n_f || model_at_k.n_u != model_final.n_u || model_at_k.n_m != model_final.n_m)
+    throw std::invalid_argument("mean_ranking_accuracy: model shape mismatch");
+  double out = 0.0;
+  check(alsncg_mean_ranking_accuracy(default_ctx(), model_at_k.n_f, model_at_k.n_u, model_at_k.n_m,
+                                     model_at_k.user_data.data(), model_at_k.item_data.data(),
+                                     model_final.user_data.data(), model_final.item_data.data(), t, &out));
+  return out;
+}
+
+}  // namespace ranking
 
 // ----------------------------------------------------------- trace CSV --
 // harness.cpp:80-127 (file format and error behaviour of the reference).

@@ -279,6 +279,10 @@ void launch_unpad_rows(Ctx* ctx, int64_t rows, int n_f, const double* padded, do
 // Multi-GPU: replicate row ranges [b[r], b[r+1]) of a row-major buffer from
 // their owning rank to all ranks (grouped in-place broadcasts over NCCL).
 void allgather_rows(Ctx* ctx, double* rows, const std::vector<int>& bounds, int ld);
+// ranking::mean_ranking_accuracy (k_ranking.cu): per-user accuracies into
+// d_q[n_u]; models in FactorModel layout (n_f doubles per user / item).
+void launch_mean_ranking(Ctx* ctx, int n_f, int n_u, int n_m, const double* d_uk, const double* d_mk,
+                         const double* d_uf, const double* d_mf, int t, double* d_q);
 // In-place sum over the ranks of n unsigned 32/64-bit counters (NCCL
 // all-reduce, or the loopback group).
 void allreduce_sum_u32(Ctx* ctx, const unsigned* send, unsigned* recv, int n);

@@ -22,6 +22,20 @@ namespace {
 // accesses index it with 32-bit offsets so they compile to LDS/STS.
 extern __shared__ __align__(16) double g_smem[];
 
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  [&]<int... Is>(std::integer_sequence<int, Is...>) { (f(std::integral_constant<int, Is>{}), ...); }(
+      std::make_integer_sequence<int, N>{});
+}
+
+// Lower-triangle block pair p -> (row, col), row-major (p = I(I+1)/2 + J).
+constexpr int tri_row(int p) {
+  int i = 0;
+  while ((i + 1) * (i + 2) / 2 <= p) ++i;
+  return i;
+}
+constexpr int tri_col(int p) { return p - tri_row(p) * (tri_row(p) + 1) / 2; }
+
 
 template <int NB, int GW>
 struct HsCfg {
@@ -139,15 +153,33 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
     }
     group_sync<GW>();
     const int bo = sb + (s & 1) * BUF + lofs;
+    if constexpr (GW == 1) {
+      // one warp owns every block pair: load each 8-row fragment of the
+      // k-step once (the A fragment of block I is the B fragment of block I)
+      // and issue all NB(NB+1)/2 DMMAs from registers -- NB shared loads per
+      // k-step instead of two per DMMA (the fused path was shared-memory bound)
 #pragma unroll 2
-    for (int kk = 0; kk < C::CH / 4; ++kk) {
-      const int base = bo + kk * 4 * C::LDS;
+      for (int kk = 0; kk < C::CH / 4; ++kk) {
+        const int base = bo + kk * 4 * C::LDS;
+        double fr[NB];
 #pragma unroll
-      for (int q = 0; q < C::Q; ++q) {
-        if (q < C::Q - 1 || warp + q * GW < C::P) {
-          const double av = g_smem[base + aoff[q]];
-          const double bv = g_smem[base + boff[q]];
-          dmma884(acc[q][0], acc[q][1], av, bv);
+        for (int b = 0; b < NB; ++b) fr[b] = g_smem[base + 8 * b];
+        static_for<C::P>([&](auto pc) {
+          constexpr int p = decltype(pc)::value;
+          dmma884(acc[p][0], acc[p][1], fr[tri_row(p)], fr[tri_col(p)]);
+        });
+      }
+    } else {
+#pragma unroll 2
+      for (int kk = 0; kk < C::CH / 4; ++kk) {
+        const int base = bo + kk * 4 * C::LDS;
+#pragma unroll
+        for (int q = 0; q < C::Q; ++q) {
+          if (q < C::Q - 1 || warp + q * GW < C::P) {
+            const double av = g_smem[base + aoff[q]];
+            const double bv = g_smem[base + boff[q]];
+            dmma884(acc[q][0], acc[q][1], av, bv);
+          }
         }
       }
     }
@@ -659,11 +691,6 @@ __device__ __forceinline__ int pidx(int I, int J) { return I * (I + 1) / 2 + J; 
 // C-fragment (16-byte) and A/B-fragment (8-byte) accesses are conflict-free.
 __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r >> 1) & 1))); }
 
-template <int N, typename F>
-__device__ __forceinline__ void static_for(F&& f) {
-  [&]<int... Is>(std::integer_sequence<int, Is...>) { (f(std::integral_constant<int, Is>{}), ...); }(
-      std::make_integer_sequence<int, N>{});
-}
 
 // ---------------------------------------------------------------------------
 // K3 v2 (k_hs_solve_ws): warp-specialised persistent solve.  One CTA per SM,
