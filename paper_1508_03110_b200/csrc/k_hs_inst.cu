@@ -284,6 +284,12 @@ __device__ __forceinline__ void init_pairs(int warp, int (&pI)[HsCfg<NB, GW>::Q]
   }
 }
 
+// Blocked elimination of one column's augmented Gram by a single warp
+// (small ranks); defined after the k_hs_solve_ws helpers it reuses.
+template <int NB>
+__device__ void solve_row_blk(const HsArgs& a, double* S, int lr, int count, int lane,
+                              double (&acc)[HsCfg<NB, 1>::Q][2]);
+
 template <int NB, int GW>
 __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
   using C = HsCfg<NB, GW>;
@@ -314,7 +320,10 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_main(HsArgs a) {
           make_double2(acc[q][0], acc[q][1]);
     return;
   }
-  solve_row<NB, GW>(a, S, lr, len, gtid, warp, lane, acc, pI, pJ);
+  if constexpr (GW == 1)
+    solve_row_blk<NB>(a, S, lr, len, lane, acc);
+  else
+    solve_row<NB, GW>(a, S, lr, len, gtid, warp, lane, acc, pI, pJ);
 }
 
 template <int NB, int GW>
@@ -341,7 +350,10 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
   }
   const int lr = a.m_row[m];
   const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
-  solve_row<NB, GW>(a, S, lr, count, gtid, warp, lane, acc, pI, pJ);
+  if constexpr (GW == 1)
+    solve_row_blk<NB>(a, S, lr, count, lane, acc);
+  else
+    solve_row<NB, GW>(a, S, lr, count, gtid, warp, lane, acc, pI, pJ);
 }
 
 // ------------------------------------------------ split path (n_f >= 31) --
@@ -737,10 +749,10 @@ struct WsList {
   int I[NB * (NB + 1) / 2];
   int K[NB * (NB + 1) / 2];
   // Y' blocks: I in (J, NB) round-robin, I = J+1 on warp 0 (needed first)
-  static constexpr WsList y(int J, int d) {
+  static constexpr WsList y(int J, int d, int DW) {
     WsList l{};
     for (int i = J + 1; i < NB; ++i)
-      if ((i - J - 1) % 3 == d) {
+      if ((i - J - 1) % DW == d) {
         l.I[l.n] = i;
         l.K[l.n] = J;
         ++l.n;
@@ -749,14 +761,14 @@ struct WsList {
   }
   // update blocks (I,K), J < K <= I < NB: (J+1,J+1) is position 0 (warp 0,
   // first); the rest in column-major order, split evenly over the 3 warps
-  static constexpr WsList u(int J, int d) {
+  static constexpr WsList u(int J, int d, int DW) {
     WsList l{};
     const int total = (NB - 1 - J) * (NB - J) / 2;
     int pos = 0;
     for (int k = J + 1; k < NB; ++k)
       for (int i = k; i < NB; ++i) {
         const int p = (i == J + 1 && k == J + 1) ? 0 : ++pos;
-        if (p * 3 / total == d) {
+        if (p * DW / total == d) {
           l.I[l.n] = i;
           l.K[l.n] = k;
           ++l.n;
@@ -777,13 +789,13 @@ struct WsList {
   }
 };
 
-template <int NB, int J, int d>
+template <int NB, int J, int d, int DW>
 struct WsY {
-  static constexpr WsList<NB> v = WsList<NB>::y(J, d);
+  static constexpr WsList<NB> v = WsList<NB>::y(J, d, DW);
 };
-template <int NB, int J, int d>
+template <int NB, int J, int d, int DW>
 struct WsU {
-  static constexpr WsList<NB> v = WsList<NB>::u(J, d);
+  static constexpr WsList<NB> v = WsList<NB>::u(J, d, DW);
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -836,9 +848,9 @@ __device__ __forceinline__ bool ws_factor(double* M, int n_f, int IR, int rl, in
 }
 
 // DMMA warp d, panel J, step 1: Y'_I = M(I,J) (-D_J^-1) into the staging area.
-template <int NB, int J, int d>
+template <int NB, int J, int d, int DW = 3>
 __device__ __forceinline__ void ws_y(double* M, int r, int q) {
-  using L = WsY<NB, J, d>;
+  using L = WsY<NB, J, d, DW>;
   if constexpr (L::v.n > 0) {
     const double* ND = M + pidx(J, J) * 64;
     const double b0 = ND[swz(q, r)], b1 = ND[swz(4 + q, r)];  // B[k][n] = ND[k][n]
@@ -856,9 +868,9 @@ __device__ __forceinline__ void ws_y(double* M, int r, int q) {
 // DMMA warp d, panel J, step 2: M(I,K) += M(I,J) Y'_K^T, four blocks per
 // batch (all loads first).  Warp 0 starts with (J+1,J+1) and then signals
 // the pivot warp through `upd`.
-template <int NB, int J, int d>
+template <int NB, int J, int d, int DW = 3>
 __device__ __forceinline__ void ws_update(double* M, int r, int q, int lane, int KP, uint64_t* upd) {
-  using L = WsU<NB, J, d>;
+  using L = WsU<NB, J, d, DW>;
   constexpr int OS = WsSolve<NB>::OFF_S;
   const int oc = swz(r, 2 * q), oa0 = swz(r, q), oa1 = swz(r, 4 + q);
   auto one = [&](auto ic) {
@@ -872,7 +884,7 @@ __device__ __forceinline__ void ws_update(double* M, int r, int q, int lane, int
   if constexpr (first) {
     one(std::integral_constant<int, 0>{});
     __syncwarp();
-    if (J + 1 < KP && lane == 0) mbar_arrive(upd);
+    if (upd != nullptr && J + 1 < KP && lane == 0) mbar_arrive(upd);
   }
   constexpr int G = 4;
   constexpr int rest = L::v.n - first;
@@ -907,6 +919,103 @@ __device__ __forceinline__ void ws_update(double* M, int r, int q, int lane, int
       }
     });
   });
+}
+
+// Back substitution by one warp after the blocked elimination:
+// x_J = D_J^-1 (w_J - sum_{I>J} M(I,J)^T x_I), w the final rhs row.
+template <int NB>
+__device__ __forceinline__ void ws_backsub(double* M, int n_f, int KP, int IR, int rl, int lane, double* out) {
+  const double* Wv = M + WsSolve<NB>::OFF_W;
+  // w lives in registers: lane l owns entries l + 32u.  Per block J:
+  // gather w_J by shuffle, x_J[n] = -(ND_J w_J)[n] in lane n (two 4-term
+  // chains), broadcast x_J, fold it into the owned entries of blocks K < J.
+  constexpr int NWR = (8 * NB + 31) / 32;
+  double wr[NWR];
+#pragma unroll
+  for (int u = 0; u < NWR; ++u) {
+    const int i = lane + 32 * u;
+    const int K = i >> 3;
+    wr[u] = i < 8 * KP ? (K < IR ? M[pidx(IR, K) * 64 + swz(rl, i & 7)] : Wv[i]) : 0.0;
+  }
+  for (int J = KP - 1; J >= 0; --J) {
+    const int u = J >> 2;  // entries 8J..8J+7 sit in register u of lanes (8J & 31)..+7
+    double wsrc = wr[0];
+#pragma unroll
+    for (int v = 1; v < NWR; ++v) wsrc = u == v ? wr[v] : wsrc;
+    const double* ND = M + pidx(J, J) * 64;
+    const int n = lane & 7;
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      t0 = fma(ND[swz(n, cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + cc), t0);
+      t1 = fma(ND[swz(n, 4 + cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + 4 + cc), t1);
+    }
+    const double x = -(t0 + t1);
+    if (lane < 8 && 8 * J + n < n_f) out[8 * J + n] = x;
+    double xr[8];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) xr[rr] = __shfl_sync(kFull, x, rr);
+#pragma unroll
+    for (int v = 0; v < NWR; ++v) {
+      const int i = lane + 32 * v;
+      if (i < 8 * J) {
+        const double* blk = M + pidx(J, i >> 3) * 64;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          a0 = fma(blk[swz(rr, i & 7)], xr[rr], a0);
+          a1 = fma(blk[swz(4 + rr, i & 7)], xr[4 + rr], a1);
+        }
+        wr[v] -= a0 + a1;
+      }
+    }
+  }
+}
+
+template <int NB>
+__device__ void solve_row_blk(const HsArgs& a, double* S, int lr, int count, int lane,
+                              double (&acc)[HsCfg<NB, 1>::Q][2]) {
+  // the warp owns every block (GW == 1): acc[p] is block p = I(I+1)/2 + J
+  const int n_f = a.n_f, ld = a.ld;
+  const int r = lane >> 2, q = lane & 3;
+  double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+  __syncwarp();  // the stage buffers are dead; the block store aliases them
+#pragma unroll
+  for (int p = 0; p < HsCfg<NB, 1>::P; ++p)
+    *reinterpret_cast<double2*>(S + p * 64 + swz(r, 2 * q)) = make_double2(acc[p][0], acc[p][1]);
+  const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
+  bool ok = shift > 0.0;
+  if (ok) {
+    __syncwarp();
+    for (int k = lane; k < n_f; k += 32) S[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;
+    __syncwarp();
+    const int KP = (n_f + 7) >> 3, IR = ld >> 3, rl = ld & 7;
+    static_for<NB>([&](auto Jc) {
+      constexpr int J = decltype(Jc)::value;
+      if (!ok || J >= KP) return;
+      ok = 8 * (J + 1) <= n_f ? ws_factor<NB, J, true>(S, n_f, IR, rl, lane)
+                              : ws_factor<NB, J, false>(S, n_f, IR, rl, lane);
+      __syncwarp();
+      if constexpr (J + 1 < NB) {
+        if (ok) {
+          ws_y<NB, J, 0, 1>(S, r, q);
+          __syncwarp();
+          ws_update<NB, J, 0, 1>(S, r, q, lane, KP, nullptr);
+          __syncwarp();
+        }
+      }
+    });
+    if (ok) {
+      ws_backsub<NB>(S, n_f, KP, IR, rl, lane, out);
+      for (int k = n_f + lane; k < ld; k += 32) out[k] = 0.0;
+      return;
+    }
+  }
+  if (lane == 0) {  // lambda*n == 0 or a non-positive pivot: least-norm fallback
+    const unsigned slot = atomicAdd(a.fb_count, 1u);
+    a.fb_list[slot] = lr;
+    atomicAdd(a.fb_total, 1u);
+  }
 }
 
 template <int NB, int d>
@@ -1084,51 +1193,7 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
     if (role != 0) probe_on = false;
 #endif
     if (role != 0) continue;
-    // ---- back substitution (pivot warp), x_J = D_J^-1 (w_J - sum_{I>J} M(I,J)^T x_I)
-    // w lives in registers: lane l owns entries l + 32u.  Per block J:
-    // gather w_J by shuffle, x_J[n] = -(ND_J w_J)[n] in lane n (two 4-term
-    // chains), broadcast x_J, fold it into the owned entries of blocks K < J.
-    constexpr int NWR = (8 * NB + 31) / 32;
-    double wr[NWR];
-#pragma unroll
-    for (int u = 0; u < NWR; ++u) {
-      const int i = lane + 32 * u;
-      const int K = i >> 3;
-      wr[u] = i < 8 * KP ? (K < IR ? M[pidx(IR, K) * 64 + swz(rl, i & 7)] : Wv[i]) : 0.0;
-    }
-    for (int J = KP - 1; J >= 0; --J) {
-      const int u = J >> 2;  // entries 8J..8J+7 sit in register u of lanes (8J & 31)..+7
-      double wsrc = wr[0];
-#pragma unroll
-      for (int v = 1; v < NWR; ++v) wsrc = u == v ? wr[v] : wsrc;
-      const double* ND = M + pidx(J, J) * 64;
-      const int n = lane & 7;
-      double t0 = 0.0, t1 = 0.0;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        t0 = fma(ND[swz(n, cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + cc), t0);
-        t1 = fma(ND[swz(n, 4 + cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + 4 + cc), t1);
-      }
-      const double x = -(t0 + t1);
-      if (lane < 8 && 8 * J + n < n_f) out[8 * J + n] = x;
-      double xr[8];
-#pragma unroll
-      for (int rr = 0; rr < 8; ++rr) xr[rr] = __shfl_sync(kFull, x, rr);
-#pragma unroll
-      for (int v = 0; v < NWR; ++v) {
-        const int i = lane + 32 * v;
-        if (i < 8 * J) {
-          const double* blk = M + pidx(J, i >> 3) * 64;
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            a0 = fma(blk[swz(rr, i & 7)], xr[rr], a0);
-            a1 = fma(blk[swz(4 + rr, i & 7)], xr[4 + rr], a1);
-          }
-          wr[v] -= a0 + a1;
-        }
-      }
-    }
+    ws_backsub<NB>(M, n_f, KP, IR, rl, lane, out);
     for (int k = n_f + lane; k < ld; k += 32) out[k] = 0.0;
     WS_PROBE(61);
 #ifdef AB2_WS_PROBE
@@ -1181,7 +1246,10 @@ template <int NB>
 void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
   constexpr int GW = Mode<NB>::GW;
   using C = HsCfg<NB, GW>;
-  if constexpr (NB <= 4) {
+#ifndef AB2_FUSED_MAX_NB
+#define AB2_FUSED_MAX_NB 4
+#endif
+  if constexpr (NB <= AB2_FUSED_MAX_NB) {
     // fused warp-per-segment kernel (Gram + solve in one pass)
     const SegPlan& P = R.plan(kind, S);
     a.seg_row = P.seg_row;
