@@ -357,181 +357,6 @@ __global__ void __launch_bounds__(HsCfg<NB, GW>::THREADS) k_hs_reduce(HsArgs a) 
 }
 
 // ------------------------------------------------ split path (n_f >= 31) --
-// K1/K2: Gram-only kernel.  The NB(NB+1)/2 lower-triangular 8x8 blocks are
-// split into GR bands of block rows (compile-time, balanced pair counts);
-// warp w owns band w / GK and every GK-th k-step (k-group w % GK).  Per
-// k-step a warp loads each needed 8-row fragment ONCE into registers (the
-// A fragment of block I equals the B fragment of block I) and issues all of
-// its band's DMMAs from registers: ~0.3 shared loads per DMMA instead of 2,
-// which is what lets the FP64 tensor pipe run near its peak.
-constexpr int kGramStage = 32;  // ratings per TMA stage in the Gram kernel
-
-template <int NB>
-struct GramShape {
-  static constexpr int P = NB * (NB + 1) / 2;
-  // ~24 block pairs per warp (48 accumulator doubles): enough register reuse
-  // per fragment load, and light enough for 3-4 CTAs per SM.
-  // <= ~48 block pairs (96 accumulator doubles) per warp; the k-steps of a
-  // stage are split over GK warps per band when there are few bands.
-  static constexpr int GR = (P + 47) / 48 < 2 ? 2 : ((P + 47) / 48 > 8 ? 8 : (P + 47) / 48);
-  static constexpr int GK = GR >= 4 ? 1 : 4 / GR;
-  static constexpr int W = GR * GK;
-  // first block row of band r (balanced by pair count)
-  static constexpr int band_start(int r) {
-    if (r <= 0) return 0;
-    if (r >= GR) return NB;
-    int acc = 0;
-    for (int I = 0; I < NB; ++I) {
-      if (acc * GR >= r * P) return I;
-      acc += I + 1;
-    }
-    return NB;
-  }
-  static constexpr int band_pairs(int r) {
-    const int a = band_start(r), b = band_start(r + 1);
-    return b * (b + 1) / 2 - a * (a + 1) / 2;
-  }
-  static constexpr int max_pairs() {
-    int m = 0;
-    for (int r = 0; r < GR; ++r) m = band_pairs(r) > m ? band_pairs(r) : m;
-    return m;
-  }
-  static constexpr int MAXP = max_pairs();
-};
-
-template <int NB, int R>
-__device__ __forceinline__ void gram_band_kstep(int base, double (&acc)[GramShape<NB>::MAXP][2]) {
-  using G = GramShape<NB>;
-  constexpr int I0 = G::band_start(R), I1 = G::band_start(R + 1);
-  double f[I1 > 0 ? I1 : 1];
-#pragma unroll
-  for (int b = 0; b < I1; ++b) f[b] = g_smem[base + 8 * b];
-  int p = 0;
-#pragma unroll
-  for (int I = I0; I < I1; ++I)
-#pragma unroll
-    for (int J = 0; J <= I; ++J) {
-      dmma884(acc[p][0], acc[p][1], f[I], f[J]);
-      ++p;
-    }
-}
-
-template <int NB, int R>
-__device__ __forceinline__ void gram_band(const HsArgs& a, int64_t beg, int len, int kgroup,
-                                          int lane, double (&acc)[GramShape<NB>::MAXP][2]) {
-  using G = GramShape<NB>;
-  using C = HsCfg<NB, G::W>;
-  constexpr int CH = kGramStage;
-  constexpr int BUF = CH * C::LDS;
-  const int gtid = threadIdx.x, warp = gtid >> 5;
-  const int ld = a.ld;
-  const int padw = C::LDS - ld;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + 2 * BUF);  // 2 mbarriers after the buffers
-  for (int e = gtid; e < 2 * CH * padw; e += C::GT) {
-    const int t = e / padw, c = e - t * padw;
-    g_smem[t * C::LDS + ld + c] = 0.0;
-  }
-  if (gtid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  // Stage s -> buffer s&1: warp 0 gathers the stage's rows with one TMA bulk
-  // copy per rating (lane t copies source row idx[t], ld*8 bytes) completing
-  // on the buffer's mbarrier; missing tail rows are zero-filled and the
-  // rating values go to column ld with ordinary stores.
-  auto issue = [&](int s) {
-    const int base = s * CH;
-    const int bo = (s & 1) * BUF;
-    const int nv = min(CH, len - base);
-    if (warp == 0) {
-      fence_proxy_async_smem();  // prior generic reads of this buffer happen-before the async writes
-      if (lane == 0) mbar_arrive_expect_tx(bar + (s & 1), static_cast<unsigned>(nv) * ld * 8);
-      __syncwarp();
-      for (int t = lane; t < nv; t += 32) {
-        const int j = a.idx[beg + base + t];
-        tma_load_1d(&g_smem[bo + t * C::LDS], a.src + static_cast<int64_t>(j) * ld,
-                    static_cast<unsigned>(ld) * 8, bar + (s & 1));
-      }
-    }
-    for (int e = gtid; e < (CH - nv) * ld; e += C::GT) {
-      const int t = nv + e / ld, c = e % ld;
-      g_smem[bo + t * C::LDS + c] = 0.0;
-    }
-    for (int t = gtid; t < CH; t += C::GT)
-      g_smem[bo + t * C::LDS + ld] = t < nv ? a.val[beg + base + t] : 0.0;
-  };
-  const int lofs = (lane & 3) * C::LDS + (lane >> 2);
-  const int nst = (len + CH - 1) / CH;
-  if (nst > 0) issue(0);
-  for (int s = 0; s < nst; ++s) {
-    if (s + 1 < nst) issue(s + 1);
-    mbar_wait(bar + (s & 1), (s >> 1) & 1);
-    __syncthreads();  // zero rows / rating column of stage s visible
-    const int bo = (s & 1) * BUF + lofs;
-#pragma unroll
-    for (int kk = kgroup; kk < CH / 4; kk += G::GK) gram_band_kstep<NB, R>(bo + kk * 4 * C::LDS, acc);
-    __syncthreads();
-  }
-}
-
-template <int NB, int R>
-__device__ __forceinline__ void gram_band_out(int kgroup, int lane, double* out,
-                                              double (&acc)[GramShape<NB>::MAXP][2]) {
-  using G = GramShape<NB>;
-  constexpr int I0 = G::band_start(R);
-  constexpr int NP = G::band_pairs(R);
-  constexpr int p0 = I0 * (I0 + 1) / 2;
-  // k-groups > 0 park their partials in shared memory; k-group 0 adds them in
-  // k-group order (deterministic) and writes the band's canonical blocks.
-  double* park = g_smem + R * (G::GK - 1) * G::MAXP * 64;
-  if (kgroup > 0) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-      *reinterpret_cast<double2*>(park + ((kgroup - 1) * G::MAXP + p) * 64 + lane * 2) =
-          make_double2(acc[p][0], acc[p][1]);
-  }
-  __syncthreads();
-  if (kgroup == 0) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      double2 v = make_double2(acc[p][0], acc[p][1]);
-      for (int g = 1; g < G::GK; ++g) {
-        const double2 u = *reinterpret_cast<const double2*>(park + ((g - 1) * G::MAXP + p) * 64 + lane * 2);
-        v.x += u.x;
-        v.y += u.y;
-      }
-      __stcs(reinterpret_cast<double2*>(out + (p0 + p) * 64 + lane * 2), v);  // streaming: keep L2 for factor rows
-    }
-  }
-}
-
-template <int NB>
-__global__ void __launch_bounds__(GramShape<NB>::W * 32)
-    k_hs_gram(HsArgs a, const int* __restrict__ seg_len, const int64_t* __restrict__ seg_beg,
-              const int* __restrict__ seg_slot, double* __restrict__ G) {
-  using GS = GramShape<NB>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int band = warp / GS::GK, kgroup = warp % GS::GK;
-  const int seg = blockIdx.x;
-  const int64_t beg = seg_beg[seg];
-  const int len = seg_len[seg];
-  double* out = G + static_cast<int64_t>(seg_slot[seg]) * GS::P * 64;
-  double acc[GS::MAXP][2];
-#pragma unroll
-  for (int p = 0; p < GS::MAXP; ++p) acc[p][0] = acc[p][1] = 0.0;
-  // one fully specialised body per band (compile-time fragment indices)
-#define AB2_BAND(R)                                              \
-  if (band == R && R < GS::GR) {                                 \
-    gram_band<NB, (R < GS::GR ? R : 0)>(a, beg, len, kgroup, lane, acc); \
-    gram_band_out<NB, (R < GS::GR ? R : 0)>(kgroup, lane, out, acc);     \
-  }
-  AB2_BAND(0) AB2_BAND(1) AB2_BAND(2) AB2_BAND(3) AB2_BAND(4) AB2_BAND(5) AB2_BAND(6) AB2_BAND(7)
-  AB2_BAND(8) AB2_BAND(9) AB2_BAND(10) AB2_BAND(11) AB2_BAND(12) AB2_BAND(13) AB2_BAND(14) AB2_BAND(15)
-#undef AB2_BAND
-}
-
 // Warp-specialised persistent Gram kernel (the split path's K1/K2).
 //  * warp GR is the producer: for every stage of every segment this CTA owns
 //    it waits for the ring slot to be released, writes the rating column and
@@ -547,21 +372,48 @@ constexpr int kWsCH = 32;
 template <int NB>
 struct WsShape {
   static constexpr int P = NB * (NB + 1) / 2;
-  // ~12 block pairs per consumer warp, 2..8 consumers
-  static constexpr int GR = P < 2 ? 1 : ((P + 11) / 12 < 2 ? 2 : ((P + 11) / 12 > 8 ? 8 : (P + 11) / 12));
+  // ~12 block pairs per consumer warp, 2..8 consumers; 16 consumers (one CTA
+  // per SM, a deeper ring) for NB > 20, where 8 warps would need > 255 registers
+  static constexpr int GR = NB > 20 ? 16 : (P < 2 ? 1 : ((P + 11) / 12 < 2 ? 2 : ((P + 11) / 12 > 8 ? 8 : (P + 11) / 12)));
   static constexpr int LDS = NB * 8 + 4;
   static constexpr int BUF = kWsCH * LDS;
   // ring depth: 2 stages from NB = 6 up -- more CTAs per SM, more consumer
   // warps on the DMMA pipe (measured 15.6 -> 15.3 ms at n_f = 100, Gram
   // 4.87 -> 4.70 ms at n_f = 50); NB = 5 keeps 3 stages
-  static constexpr int STAGES = NB >= 6 ? 2 : 3;
-  static constexpr int p_begin(int r) { return r * P / GR; }
-  static constexpr int row_of(int p) {
-    int i = 0;
-    while ((i + 1) * (i + 2) / 2 <= p) ++i;
-    return i;
+  static constexpr int STAGES = NB > 20 ? 4 : (NB >= 6 ? 2 : 3);
+  // NB > 20: the pairs are split over NPART = 2 CTAs (each gathers every
+  // rating of the segment and accumulates half of the pairs): the 351 pair
+  // accumulators of NB = 26 alone would fill an SM's register file.  Consumer
+  // R of part h is virtual consumer h * GR + R.
+  static constexpr int NPART = NB > 20 ? 2 : 1;
+#ifndef AB2_WS_KUNROLL_BIG
+#define AB2_WS_KUNROLL_BIG 1
+#endif
+  static constexpr int KUNROLL = NB >= 17 ? AB2_WS_KUNROLL_BIG : kWsCH / 4;  // k-steps unrolled per stage
+  static constexpr int p_begin(int r) { return r * P / (GR * NPART); }
+  // Order in which block pairs are dealt to the consumers: bands of H block
+  // rows, column by column inside a band.  H = 1 is the canonical row-major
+  // order; H = 4 (NB > 20) makes a warp's ~22 consecutive pairs a ~4 x 6 tile,
+  // so it needs ~10 fragments per k-step instead of ~23.
+  static constexpr int H = NB > 20 ? 4 : 1;
+  struct Order {
+    int i[P], j[P];
+  };
+  static constexpr Order make_order() {
+    Order o{};
+    int c = 0;
+    for (int b0 = 0; b0 < NB; b0 += H)
+      for (int j = 0; j < (b0 + H < NB ? b0 + H : NB); ++j)
+        for (int i = (b0 > j ? b0 : j); i < (b0 + H < NB ? b0 + H : NB); ++i) {
+          o.i[c] = i;
+          o.j[c] = j;
+          ++c;
+        }
+    return o;
   }
-  static constexpr int col_of(int p) { return p - row_of(p) * (row_of(p) + 1) / 2; }
+  static constexpr Order order = make_order();
+  static constexpr int row_of(int p) { return order.i[p]; }
+  static constexpr int col_of(int p) { return order.j[p]; }
   static constexpr bool needs(int r, int b) {
     for (int p = p_begin(r); p < p_begin(r + 1); ++p)
       if (row_of(p) == b || col_of(p) == b) return true;
@@ -569,7 +421,7 @@ struct WsShape {
   }
   static constexpr int max_pairs() {
     int m = 0;
-    for (int r = 0; r < GR; ++r) m = p_begin(r + 1) - p_begin(r) > m ? p_begin(r + 1) - p_begin(r) : m;
+    for (int r = 0; r < GR * NPART; ++r) m = p_begin(r + 1) - p_begin(r) > m ? p_begin(r + 1) - p_begin(r) : m;
     return m;
   }
   static constexpr int MAXP = max_pairs();
@@ -583,12 +435,14 @@ __device__ __forceinline__ void ws_kstep(int base, double (&acc)[WsShape<NB>::MA
   using S = WsShape<NB>;
   constexpr int p0 = S::p_begin(R), p1 = S::p_begin(R + 1);
   double f[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b)
-    if (S::needs(R, b)) f[b] = g_smem[base + 8 * b];
-#pragma unroll
-  for (int p = p0; p < p1; ++p)
+  static_for<NB>([&](auto bc) {
+    constexpr int b = decltype(bc)::value;
+    if constexpr (S::needs(R, b)) f[b] = g_smem[base + 8 * b];
+  });
+  static_for<p1 - p0>([&](auto pc) {
+    constexpr int p = p0 + decltype(pc)::value;
     dmma884(acc[p - p0][0], acc[p - p0][1], f[S::row_of(p)], f[S::col_of(p)]);
+  });
 }
 
 template <int NB, int R>
@@ -615,15 +469,20 @@ __device__ __forceinline__ void ws_consumer(const int* __restrict__ seg_len,
       buf = it % S::STAGES;
       if (s > 0) mbar_wait(full + buf, (it / S::STAGES) & 1);
       const int bo = buf * S::BUF + lofs;
-#pragma unroll
+      // every consumer warp runs its own code: for large NB the fully
+      // unrolled stage loops of an SM's warps overflow the instruction cache
+      // (measured at NB = 26: 85 % of stall samples "no instruction")
+#pragma unroll(S::KUNROLL)
       for (int kk = 0; kk < kWsCH / 4; ++kk) ws_kstep<NB, R>(bo + kk * 4 * S::LDS, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + buf);
     }
-    double* out = G + static_cast<int64_t>(seg_slot[seg]) * S::P * 64 + p0 * 64 + lane * 2;
-#pragma unroll
-    for (int p = 0; p < np; ++p)
-      __stcs(reinterpret_cast<double2*>(out + p * 64), make_double2(acc[p][0], acc[p][1]));
+    double* out = G + static_cast<int64_t>(seg_slot[seg]) * S::P * 64 + lane * 2;
+    static_for<np>([&](auto pc) {  // stored at the canonical pair index
+      constexpr int p = decltype(pc)::value;
+      constexpr int pc_idx = S::row_of(p0 + p) * (S::row_of(p0 + p) + 1) / 2 + S::col_of(p0 + p);
+      __stcs(reinterpret_cast<double2*>(out + pc_idx * 64), make_double2(acc[p][0], acc[p][1]));
+    });
   }
 }
 
@@ -635,6 +494,8 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
   using S = WsShape<NB>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = a.ld;
+  const int part = S::NPART == 1 ? 0 : static_cast<int>(blockIdx.x) % S::NPART;
+  next_seg += part;  // one segment counter per part
   uint64_t* full = reinterpret_cast<uint64_t*>(g_smem + S::STAGES * S::BUF);
   uint64_t* empty = full + S::STAGES;
   int* hdr = reinterpret_cast<int*>(empty + S::STAGES);  // segment id per stage
@@ -690,10 +551,16 @@ __global__ void __launch_bounds__((WsShape<NB>::GR + 1) * 32)
     return;
   }
   // ------------------------------------------ consumers (compile-time band)
-#define AB2_WS(R)                                                                           \
-  if (warp == R && R < S::GR)                                                               \
-    ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, hdr, lane);
+#define AB2_WS(R)                                                                              \
+  if (warp == R && R < S::GR) {                                                                \
+    if (part == 0)                                                                             \
+      ws_consumer<NB, (R < S::GR ? R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, hdr, lane); \
+    else if constexpr (S::NPART > 1)                                                           \
+      ws_consumer<NB, (R < S::GR ? S::GR + R : 0)>(seg_len, seg_slot, n_seg, G, full, empty, hdr, \
+                                                   lane);                                      \
+  }
   AB2_WS(0) AB2_WS(1) AB2_WS(2) AB2_WS(3) AB2_WS(4) AB2_WS(5) AB2_WS(6) AB2_WS(7)
+  AB2_WS(8) AB2_WS(9) AB2_WS(10) AB2_WS(11) AB2_WS(12) AB2_WS(13) AB2_WS(14) AB2_WS(15)
 #undef AB2_WS
 }
 
@@ -706,7 +573,8 @@ __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r 
 
 // ---------------------------------------------------------------------------
 // K3 v2 (k_hs_solve_ws): warp-specialised persistent solve.  One CTA per SM,
-// TEAMS teams of four warps, one column in flight per team (the team's
+// TEAMS teams of 1 + DW warps (DW = 3 for n_f <= 120; 6 or 12 DMMA warps when
+// only two or one column fit per SM), one column in flight per team (the team's
 // shared block store holds that column's lower-triangular augmented Gram).
 // The measured constraint (profiles/fp64_latency.txt): DFMA and DMMA share the
 // FP64 datapath of an SM sub-partition (SMSP), and a dependent scalar FP64
@@ -739,7 +607,14 @@ struct WsSolve {
   static constexpr int TEAM_BYTES = TEAM_D * 8;
   static constexpr int FIT = (227 * 1024) / TEAM_BYTES;
   static constexpr int TEAMS = FIT > 6 ? 6 : (FIT < 1 ? 1 : FIT);
-  static constexpr int THREADS = TEAMS * 128;
+  // Large ranks fit one or two columns per SM: their teams get more DMMA
+  // warps (WPS per SMSP 1-3) so the SM still holds 16 warps.  The CTA has
+  // TEAMS * WPS warps on every SMSP; on SMSP 0 only one per team works (the
+  // pivot warp), the others exit after the prologue.
+  static constexpr int WPS = TEAMS == 1 ? 4 : (TEAMS == 2 ? 2 : 1);
+  static constexpr int DW = 3 * WPS;            // DMMA warps per team
+  static constexpr int ACT = (1 + DW) * 32;     // working threads per team
+  static constexpr int THREADS = TEAMS * WPS * 128;
 };
 
 // Compile-time work lists of DMMA warp d for panel J.
@@ -1018,7 +893,7 @@ __device__ void solve_row_blk(const HsArgs& a, double* S, int lr, int count, int
   }
 }
 
-template <int NB, int d>
+template <int NB, int d, int DW>
 __device__ __forceinline__ void ws_dmma_role(double* M, int KP, int team, int lane, uint64_t* diag,
                                              uint64_t* upd, unsigned& ph_diag, volatile int* fail,
                                              unsigned long long* probe = nullptr) {
@@ -1034,10 +909,10 @@ __device__ __forceinline__ void ws_dmma_role(double* M, int KP, int team, int la
       return;
     }
     if constexpr (J + 1 < NB) {
-      ws_y<NB, J, d>(M, r, q);
-      named_bar(1 + team, 96);
-      ws_update<NB, J, d>(M, r, q, lane, KP, upd);
-      named_bar(1 + team, 96);
+      ws_y<NB, J, d, DW>(M, r, q);
+      named_bar(1 + team, 32 * DW);
+      ws_update<NB, J, d, DW>(M, r, q, lane, KP, upd);
+      named_bar(1 + team, 32 * DW);
       if (probe && lane == 0 && J < 19) probe[4 + 3 * J] = clock64();
     }
   });
@@ -1063,7 +938,8 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
   __shared__ uint64_t bars[T][2];  // [0] inverse ready (pivot -> DMMA), [1] next diagonal updated
   __shared__ int team_col[T];
   __shared__ int team_fail[T];
-  __shared__ int slot_of[T * 4];
+  constexpr int WPS = W::WPS, DW = W::DW, NW = T * WPS * 4;
+  __shared__ int slot_of[NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Roles by SM sub-partition: the warp's hardware slot (%warpid) decides its
   // SMSP (slot % 4), not its index in the CTA (measured: CTA warp 0 lands on
@@ -1076,10 +952,11 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
     if (lane == 0) slot_of[warp] = static_cast<int>(wid);
   }
   __syncthreads();
-  int team = warp >> 2, role = warp & 3;
+  // role: 0 = pivot warp, 1..DW = DMMA warp role-1, > DW = idle (SMSP 0 spares)
+  int team = warp / (WPS * 4), role = warp % (WPS * 4);
   {
     int cnt[4] = {0, 0, 0, 0}, my_s = 0, my_rank = 0;
-    for (int w = 0; w < T * 4; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const int sp = slot_of[w] & 3;
       if (w == warp) {
         my_s = sp;
@@ -1087,9 +964,10 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
       }
       ++cnt[sp];
     }
-    if (cnt[0] == T && cnt[1] == T && cnt[2] == T && cnt[3] == T) {
-      team = my_rank;
-      role = my_s;
+    if (cnt[0] == T * WPS && cnt[1] == T * WPS && cnt[2] == T * WPS && cnt[3] == T * WPS) {
+      team = my_rank % T;
+      const int sub = my_rank / T;
+      role = my_s == 0 ? (sub == 0 ? 0 : DW + 1) : 1 + (my_s - 1) * WPS + sub;
     }
   }
   const int ttid = role * 32 + lane;
@@ -1106,6 +984,7 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
     mbar_fence_init();
   }
   __syncthreads();
+  if (role > DW) return;  // spare warp on the pivot SMSP: takes no barrier below
   unsigned ph_diag = 0, ph_upd = 0;
 #ifdef AB2_WS_PROBE
   bool probe_on = team == 0 && blockIdx.x < 64;
@@ -1116,12 +995,12 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
   }
 #endif
   for (;;) {
-    named_bar(team_bar, 128);  // the previous column's smem reads are done
+    named_bar(team_bar, W::ACT);  // the previous column's smem reads are done
     if (ttid == 0) {
       team_col[team] = atomicAdd(next_col, 1);
       team_fail[team] = 0;
     }
-    named_bar(team_bar, 128);
+    named_bar(team_bar, W::ACT);
     const int c = team_col[team];
     if (c >= s.nrows) break;
     if (role == 0) WS_PROBE(0);
@@ -1129,7 +1008,7 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
     double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
     const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
     if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
-      for (int k = ttid; k < ld; k += 128) out[k] = 0.0;
+      for (int k = ttid; k < ld; k += W::ACT) out[k] = 0.0;
       continue;
     }
     const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
@@ -1142,11 +1021,11 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
     }
     {  // heavy rows were folded into their first slot by k_hs_slot_reduce
       const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * W::P * 64 + lane * 2;
-      for (int p = role; p < W::P; p += 4) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
+      for (int p = role; p < W::P; p += 1 + DW) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
       cp_async_commit();
       cp_async_wait<0>();
     }
-    named_bar(team_bar, 128);
+    named_bar(team_bar, W::ACT);
     if (role == 0) WS_PROBE(1);
     if (role == 0) {
       for (int k = lane; k < n_f; k += 32) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;  // als.cpp:58-59
@@ -1168,19 +1047,19 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
         if (lane == 0) mbar_arrive(&bars[team][0]);
         ++ph_diag;
       });
-    } else if (role == 1) {
-#ifdef AB2_WS_PROBE
-      ws_dmma_role<NB, 0>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team],
-                          probe_on ? &g_ws_probe[blockIdx.x][0] : nullptr);
-#else
-      ws_dmma_role<NB, 0>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
-#endif
-    } else if (role == 2) {
-      ws_dmma_role<NB, 1>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
     } else {
-      ws_dmma_role<NB, 2>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
+      static_for<DW>([&](auto dc) {
+        constexpr int d = decltype(dc)::value;
+        if (role != 1 + d) return;
+#ifdef AB2_WS_PROBE
+        ws_dmma_role<NB, d, DW>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team],
+                                d == 0 && probe_on ? &g_ws_probe[blockIdx.x][0] : nullptr);
+#else
+        ws_dmma_role<NB, d, DW>(M, KP, team, lane, &bars[team][0], &bars[team][1], ph_diag, &team_fail[team]);
+#endif
+      });
     }
-    named_bar(team_bar, 128);  // every panel of this column is done
+    named_bar(team_bar, W::ACT);  // every panel of this column is done
     if (role == 0) WS_PROBE(60);
     if (team_fail[team]) {
       if (ttid == 0) {
@@ -1238,10 +1117,6 @@ struct Mode {
 };
 
 constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
-// compile-time kernel choice: only the kernels a rank uses are instantiated
-template <int NB>
-constexpr bool kGramWs = NB <= 20;                // warp-specialised persistent Gram
-
 template <int NB>
 void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
   constexpr int GW = Mode<NB>::GW;
@@ -1281,17 +1156,10 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
   } else {
     const size_t slot_bytes = sizeof(double) * C::P * 64;
     const HsPlan& P = R.hs_plan(kind, S, std::max<int64_t>(1, kGramBudget / slot_bytes));
-    using GS = GramShape<NB>;
-    using GC = HsCfg<NB, GS::W>;
-    const size_t gsmem = sizeof(double) * std::max<size_t>(2 * kGramStage * GC::LDS + 2,
-                                                           size_t(GS::GR) * (GS::GK - 1) * GS::MAXP * 64);
     // per-device attribute / occupancy cache (Ctx::prepare_kernel)
-    int gram_per_sm = 1;
-    if constexpr (kGramWs<NB>)
-      gram_per_sm = ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_gram_ws<NB>), 227 * 1024,
-                                        (WsShape<NB>::GR + 1) * 32, WsShape<NB>::smem_bytes());
-    else
-      ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_gram<NB>), 227 * 1024, 0, 0);
+    const int gram_per_sm =
+        ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_gram_ws<NB>), 227 * 1024,
+                            (WsShape<NB>::GR + 1) * 32, WsShape<NB>::smem_bytes());
     ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_solve_ws<NB>),
                         WsSolve<NB>::TEAMS * WsSolve<NB>::TEAM_BYTES, 0, 0);
     double* G = static_cast<double*>(ctx->scratch(2, slot_bytes * std::max(P.max_batch_slots, 1)));
@@ -1304,22 +1172,16 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
         AB2_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
         ctx->side_join = false;
       }
-      if constexpr (kGramWs<NB>) {
-        if (b.seg1 > b.seg0) {
-          using WS = WsShape<NB>;
-          const int nseg = b.seg1 - b.seg0;
-          const int grid = std::min(nseg, gram_per_sm * ctx->sm_count);  // persistent CTAs
-          int* next_seg = static_cast<int*>(ctx->scratch(8, sizeof(int)));
-          AB2_CUDA(cudaMemsetAsync(next_seg, 0, sizeof(int), ctx->stream));
-          const int tok = ctx->begin_launch("halfsweep_gram");
-          k_hs_gram_ws<NB><<<grid, (WS::GR + 1) * 32, WS::smem_bytes(), ctx->stream>>>(
-              a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G, next_seg);
-          ctx->end_launch(tok);
-        }
-      } else if (b.seg1 > b.seg0) {
+      if (b.seg1 > b.seg0) {
+        using WS = WsShape<NB>;
+        const int nseg = b.seg1 - b.seg0;
+        // persistent CTAs, the same number for every part
+        const int grid = WS::NPART * std::min(nseg, std::max(gram_per_sm * ctx->sm_count / WS::NPART, 1));
+        int* next_seg = static_cast<int*>(ctx->scratch(8, WS::NPART * sizeof(int)));
+        AB2_CUDA(cudaMemsetAsync(next_seg, 0, WS::NPART * sizeof(int), ctx->stream));
         const int tok = ctx->begin_launch("halfsweep_gram");
-        k_hs_gram<NB><<<b.seg1 - b.seg0, GS::W * 32, gsmem, ctx->stream>>>(
-            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, G);
+        k_hs_gram_ws<NB><<<grid, (WS::GR + 1) * 32, WS::smem_bytes(), ctx->stream>>>(
+            a, P.seg_len + b.seg0, P.seg_beg + b.seg0, P.seg_slot + b.seg0, nseg, G, next_seg);
         ctx->end_launch(tok);
       }
       if (ctx->side_work) {  // independent side work overlaps this batch's solve
