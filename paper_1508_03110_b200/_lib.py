@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libalsncg_b200.so")
+LIB_PATH = os.environ.get("ALSNCG_LIB") or os.path.join(HERE, "libalsncg_b200.so")  # ALSNCG_LIB: development A/B builds
 
 OK, EINVAL, EDATA, EDUP, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED, ELOGIC = range(9)
 

@@ -386,10 +386,9 @@ struct WsShape {
   // accumulators of NB = 26 alone would fill an SM's register file.  Consumer
   // R of part h is virtual consumer h * GR + R.
   static constexpr int NPART = NB > 20 ? 2 : 1;
-#ifndef AB2_WS_KUNROLL_BIG
-#define AB2_WS_KUNROLL_BIG 1
-#endif
-  static constexpr int KUNROLL = NB >= 17 ? AB2_WS_KUNROLL_BIG : kWsCH / 4;  // k-steps unrolled per stage
+  // measured (Gram ms per iteration, config-1 matrix): NB = 16 28.3 -> 24.4 with 4,
+  // NB = 26 218 -> 57 with 1; NB <= 13 is fastest fully unrolled
+  static constexpr int KUNROLL = NB >= 17 ? 1 : (NB >= 14 ? 4 : kWsCH / 4);  // k-steps unrolled per stage
   static constexpr int p_begin(int r) { return r * P / (GR * NPART); }
   // Order in which block pairs are dealt to the consumers: bands of H block
   // rows, column by column inside a band.  H = 1 is the canonical row-major
@@ -1081,6 +1080,84 @@ __global__ void __launch_bounds__(WsSolve<NB>::THREADS, 1)
   }
 }
 
+// K3 for small ranks (k_hs_solve_1w): one warp per column, the same blocked
+// elimination run by that warp alone (diagonal inverse, DMMA TRSM and update,
+// shuffle back substitution) with no inter-warp hand-off.  A column's block
+// store is small here (18 KB at n_f = 50), so 10-16 columns are in flight per
+// SM instead of the 6 team columns of k_hs_solve_ws, whose per-panel
+// hand-offs (~4.5 k cycles per panel whatever NB is) dominate when the panels
+// carry only a handful of DMMAs.
+template <int NB>
+struct OneWarpSolve {
+  static constexpr int COL_D = WsSolve<NB>::TEAM_D;
+  static constexpr int FIT = (227 * 1024) / (COL_D * 8);
+  static constexpr int WARPS = FIT > 16 ? 16 : (FIT < 1 ? 1 : FIT);
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr size_t smem_bytes() { return size_t(WARPS) * COL_D * 8; }
+};
+
+template <int NB>
+__global__ void __launch_bounds__(OneWarpSolve<NB>::THREADS, 1)
+    k_hs_solve_1w(HsArgs a, SolveArgs s, int* __restrict__ next_col) {
+  using W = WsSolve<NB>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* M = g_smem + static_cast<size_t>(warp) * W::TEAM_D;
+  const int n_f = a.n_f, ld = a.ld;
+  const int KP = (n_f + 7) >> 3;
+  const int IR = ld >> 3, rl = ld & 7;
+  const int r = lane >> 2, q = lane & 3;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(next_col, 1);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= s.nrows) break;
+    const int lr = s.row0 + c;
+    double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
+    const int count = static_cast<int>(a.ptr[lr + 1] - a.ptr[lr]);
+    if (count == 0) {  // parallel.cpp:175 -- empty column stays zero
+      for (int k = lane; k < ld; k += 32) out[k] = 0.0;
+      continue;
+    }
+    const double shift = a.lambda * static_cast<double>(count);  // als.cpp:58
+    bool ok = shift > 0.0;
+    if (ok) {
+      __syncwarp();  // the previous column's reads of the block store are done
+      const double* base = s.G + static_cast<int64_t>(s.row_slot0[lr]) * W::P * 64 + lane * 2;
+#pragma unroll 4
+      for (int p = 0; p < W::P; ++p) cp_async16(M + p * 64 + swz(r, 2 * q), base + p * 64);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+      for (int k = lane; k < n_f; k += 32) M[pidx(k >> 3, k >> 3) * 64 + swz(k & 7, k & 7)] += shift;  // als.cpp:58-59
+      __syncwarp();
+      static_for<NB>([&](auto Jc) {
+        constexpr int J = decltype(Jc)::value;
+        if (!ok || J >= KP) return;
+        ok = 8 * (J + 1) <= n_f ? ws_factor<NB, J, true>(M, n_f, IR, rl, lane)
+                                : ws_factor<NB, J, false>(M, n_f, IR, rl, lane);
+        __syncwarp();
+        if constexpr (J + 1 < NB) {
+          if (ok) {
+            ws_y<NB, J, 0, 1>(M, r, q);
+            __syncwarp();
+            ws_update<NB, J, 0, 1>(M, r, q, lane, KP, nullptr);
+            __syncwarp();
+          }
+        }
+      });
+      if (ok) {
+        ws_backsub<NB>(M, n_f, KP, IR, rl, lane, out);
+        for (int k = n_f + lane; k < ld; k += 32) out[k] = 0.0;
+        continue;
+      }
+    }
+    if (lane == 0) {  // lambda*n == 0 or a non-positive pivot: least-norm fallback
+      a.fb_list[atomicAdd(a.fb_count, 1u)] = lr;
+      atomicAdd(a.fb_total, 1u);
+    }
+  }
+}
+
 // Heavy rows: fold a row's partial Gram slots into its first slot, in slot
 // order (deterministic; every load of a thread is independent, so all slots
 // of a row are in flight at once).  One thread per double2 of one row.
@@ -1117,6 +1194,19 @@ struct Mode {
 };
 
 constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
+
+// Largest block count solved by k_hs_solve_1w (one warp per column); above it
+// the warp-specialised team kernel.  ALSNCG_SOLVE_1W_MAX overrides (development A/B).
+#ifndef AB2_SOLVE_1W_MAX_NB
+#define AB2_SOLVE_1W_MAX_NB 10
+#endif
+inline int solve_1w_max_nb() {
+  static const int v = [] {
+    const char* e = std::getenv("ALSNCG_SOLVE_1W_MAX");
+    return e ? std::atoi(e) : AB2_SOLVE_1W_MAX_NB;
+  }();
+  return v;
+}
 template <int NB>
 void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
   constexpr int GW = Mode<NB>::GW;
@@ -1210,7 +1300,13 @@ void run_hs_impl(Ctx* ctx, DevRatings& R, int kind, HsArgs& a, int S) {
       using WSV = WsSolve<NB>;
       const int grid = std::min(s.nrows, ctx->sm_count);  // persistent: one CTA per SM
       const int tok = ctx->begin_launch("halfsweep_solve");
-      k_hs_solve_ws<NB><<<grid, WSV::THREADS, WSV::TEAMS * WSV::TEAM_BYTES, ctx->stream>>>(a, s, next_col);
+      if (NB <= solve_1w_max_nb()) {
+        using OW = OneWarpSolve<NB>;
+        ctx->prepare_kernel(reinterpret_cast<const void*>(k_hs_solve_1w<NB>), static_cast<int>(OW::smem_bytes()), 0, 0);
+        k_hs_solve_1w<NB><<<grid, OW::THREADS, OW::smem_bytes(), ctx->stream>>>(a, s, next_col);
+      } else {
+        k_hs_solve_ws<NB><<<grid, WSV::THREADS, WSV::TEAMS * WSV::TEAM_BYTES, ctx->stream>>>(a, s, next_col);
+      }
       ctx->end_launch(tok);
     }
   }
