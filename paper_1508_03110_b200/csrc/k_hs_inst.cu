@@ -811,11 +811,16 @@ __device__ __forceinline__ void ws_backsub(double* M, int n_f, int KP, int IR, i
     const int K = i >> 3;
     wr[u] = i < 8 * KP ? (K < IR ? M[pidx(IR, K) * 64 + swz(rl, i & 7)] : Wv[i]) : 0.0;
   }
-  for (int J = KP - 1; J >= 0; --J) {
-    const int u = J >> 2;  // entries 8J..8J+7 sit in register u of lanes (8J & 31)..+7
-    double wsrc = wr[0];
-#pragma unroll
-    for (int v = 1; v < NWR; ++v) wsrc = u == v ? wr[v] : wsrc;
+  // The block loop is unrolled and x is stored after it: a store of x_J to
+  // `out` inside the loop (which the compiler must assume may alias the block
+  // store) pins the next block's loads behind the dependent chain.
+  double xk[NB];  // x_J[lane & 7], kept by every lane
+  static_for<NB>([&](auto Jc) {
+    constexpr int J = NB - 1 - decltype(Jc)::value;
+    xk[J] = 0.0;
+    if (J >= KP) return;
+    constexpr int u = J >> 2;  // entries 8J..8J+7 sit in register u of lanes (8J & 31)..+7
+    const double wsrc = wr[u];
     const double* ND = M + pidx(J, J) * 64;
     const int n = lane & 7;
     double t0 = 0.0, t1 = 0.0;
@@ -825,14 +830,14 @@ __device__ __forceinline__ void ws_backsub(double* M, int n_f, int KP, int IR, i
       t1 = fma(ND[swz(n, 4 + cc)], __shfl_sync(kFull, wsrc, ((8 * J) & 31) + 4 + cc), t1);
     }
     const double x = -(t0 + t1);
-    if (lane < 8 && 8 * J + n < n_f) out[8 * J + n] = x;
+    xk[J] = x;
     double xr[8];
 #pragma unroll
     for (int rr = 0; rr < 8; ++rr) xr[rr] = __shfl_sync(kFull, x, rr);
 #pragma unroll
     for (int v = 0; v < NWR; ++v) {
       const int i = lane + 32 * v;
-      if (i < 8 * J) {
+      if (32 * v < 8 * J && i < 8 * J) {
         const double* blk = M + pidx(J, i >> 3) * 64;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -843,6 +848,11 @@ __device__ __forceinline__ void ws_backsub(double* M, int n_f, int KP, int IR, i
         wr[v] -= a0 + a1;
       }
     }
+  });
+  if (lane < 8) {
+#pragma unroll
+    for (int J = 0; J < NB; ++J)
+      if (J < KP && 8 * J + lane < n_f) out[8 * J + lane] = xk[J];
   }
 }
 
