@@ -66,8 +66,8 @@ __host__ __device__ constexpr size_t hs_group_doubles(int ld) {
   const int lda = (ld + 1) | 1;
   const size_t mat = C::PACKED ? static_cast<size_t>(ld + 1) * (ld + 2) / 2
                                : static_cast<size_t>(ld + 1) * lda;
-  const size_t body = stage > mat ? stage : mat;
-  return body + 2 * static_cast<size_t>(C::MAXF);  // + dinv[], w[]
+  const size_t body = ((stage > mat ? stage : mat) + 1) & ~static_cast<size_t>(1);
+  return body + 2 * static_cast<size_t>(C::MAXF) + 2;  // + dinv[], w[], two stage mbarriers
 }
 
 template <bool PACKED>
@@ -101,20 +101,59 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
   const int nch = ld >> 1;  // 16-byte chunks per source row
   const int padw = C::LDS - ld;
   // zero the pad columns (ld .. LDS) of both buffers once; column ld carries r
+  // divisions by the run-time nch / padw as one multiply-high: x / d ==
+  // umulhi(x, ceil(2^32 / d)) for x * d < 2^32 (d = 1 handled apart)
+  const unsigned inv_nch = nch > 1 ? 0xffffffffu / static_cast<unsigned>(nch) + 1u : 0u;
+  const unsigned inv_padw = padw > 1 ? 0xffffffffu / static_cast<unsigned>(padw) + 1u : 0u;
   for (int e = gtid; e < 2 * C::CH * padw; e += C::GT) {
-    const int t = e / padw, c = e - t * padw;  // t indexes rows of both buffers
+    const int t = padw > 1 ? static_cast<int>(__umulhi(static_cast<unsigned>(e), inv_padw)) : e;  // row of both buffers
+    const int c = e - t * padw;
     g_smem[sb + t * C::LDS + ld + c] = 0.0;
   }
   group_sync<GW>();
   // Each warp loads the stage's CH indices with one coalesced load (lane t
   // holds rating t) and hands them out by shuffle, so every cp.async of the
   // stage issues after a single index-load latency.
+  // GW == 1 (the fused path): lane t gathers rating t's source row with one
+  // TMA bulk copy completing on the stage's mbarrier -- one instruction per
+  // rating instead of ld/2 16-byte cp.async chunks with their index math.
+  // Measured (fused ms per iteration, config-1 matrix): f = 25 2.63 -> 2.37,
+  // f = 30 2.73 -> 2.39, but f = 16 1.55 -> 1.62 and f = 10 1.37 -> 1.47 (rows
+  // under ~150 bytes: the per-copy cost outweighs the chunk loop), hence NB >= 4.
+  constexpr bool kTma = GW == 1 && NB >= 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(g_smem + sb + hs_group_doubles<NB, GW>(ld) - 2);
+  if constexpr (kTma) {
+    if (lane == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 1, 1);
+      mbar_fence_init();
+    }
+  }
   auto issue = [&](int s, int bo) {
     const int base = s * C::CH;
     const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
+    if constexpr (kTma) {
+      const int nv = min(C::CH, len - base);
+      if (lane < C::CH) {
+        double* row = &g_smem[bo + lane * C::LDS];
+        if (lane < nv) {
+          cp_async8(row + ld, a.val + beg + base + lane);
+        } else {
+          for (int c = 0; c < ld; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(0.0, 0.0);
+          row[ld] = 0.0;
+        }
+      }
+      if (lane == 0) mbar_arrive_expect_tx(bars + (s & 1), static_cast<unsigned>(nv) * ld * 8);
+      __syncwarp();
+      if (lane < nv)
+        tma_load_1d(&g_smem[bo + lane * C::LDS], a.src + static_cast<int64_t>(jv) * ld,
+                    static_cast<unsigned>(ld) * 8, bars + (s & 1));
+      return;
+    }
     for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
       const int c = c0 + gtid;
-      const int t = min(c / nch, C::CH - 1), k = c - t * nch;
+      const int t = min(nch > 1 ? static_cast<int>(__umulhi(static_cast<unsigned>(c), inv_nch)) : c, C::CH - 1);
+      const int k = c - t * nch;
       const int j = __shfl_sync(kFull, jv, t);
       if (c < C::CH * nch) {
         double* dst = &g_smem[bo + t * C::LDS + 2 * k];
@@ -151,6 +190,7 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
     } else {
       cp_async_wait<0>();
     }
+    if constexpr (kTma) mbar_wait(bars + (s & 1), (s >> 1) & 1);
     group_sync<GW>();
     const int bo = sb + (s & 1) * BUF + lofs;
     if constexpr (GW == 1) {
@@ -198,7 +238,7 @@ __device__ __forceinline__ void solve_row(const HsArgs& a, double* S, int lr, in
   const int n_f = a.n_f, ld = a.ld;
   const int lda = (ld + 1) | 1;
   double* A = S;
-  const size_t body = hs_group_doubles<NB, GW>(ld) - 2 * C::MAXF;
+  const size_t body = hs_group_doubles<NB, GW>(ld) - 2 * C::MAXF - 2;
   double* dinv = S + body;
   double* w = dinv + C::MAXF;
   double* out = a.out + static_cast<int64_t>(a.row0 + lr) * ld;
