@@ -150,6 +150,23 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
                     static_cast<unsigned>(ld) * 8, bars + (s & 1));
       return;
     }
+    if (GW == 1 && nch <= 8) {
+      // short rows: 4 or 8 lanes per rating, chunk = lane within the rating's
+      // lanes -- shifts and masks only (the generic loop below spends ~70
+      // instructions per trip on its (rating, chunk) arithmetic)
+      const int sh = nch <= 4 ? 2 : 3;
+      const int k = lane & ((1 << sh) - 1);
+      for (int t = lane >> sh; t < C::CH; t += 32 >> sh) {
+        const int j = __shfl_sync(kFull, jv, t);
+        if (k < nch) {
+          double* dst = &g_smem[bo + t * C::LDS + 2 * k];
+          if (base + t < len)
+            cp_async16(dst, a.src + static_cast<int64_t>(j) * ld + 2 * k);
+          else
+            *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+        }
+      }
+    } else
     for (int c0 = 0; c0 < C::CH * nch; c0 += C::GT) {
       const int c = c0 + gtid;
       const int t = min(nch > 1 ? static_cast<int>(__umulhi(static_cast<unsigned>(c), inv_nch)) : c, C::CH - 1);
