@@ -129,9 +129,14 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
       mbar_fence_init();
     }
   }
-  auto issue = [&](int s, int bo) {
+  // indices of stage s: loaded one stage before they are needed, so the
+  // gathers of a stage never wait on their own index load
+  auto load_idx = [&](int s) {
     const int base = s * C::CH;
-    const int jv = (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
+    return (lane < C::CH && base + lane < len) ? a.idx[beg + base + lane] : 0;
+  };
+  auto issue = [&](int s, int bo, int jv) {
+    const int base = s * C::CH;
     if constexpr (kTma) {
       const int nv = min(C::CH, len - base);
       if (lane < C::CH) {
@@ -197,11 +202,14 @@ __device__ __forceinline__ void gram_segment(const HsArgs& a, int sb, int64_t be
   }
   const int lofs = (lane & 3) * C::LDS + (lane >> 2);
   const int nst = (len + C::CH - 1) / C::CH;
-  if (nst > 0) issue(0, sb);
+  int jn = load_idx(0);
+  if (nst > 0) issue(0, sb, jn);
   cp_async_commit();
+  jn = load_idx(1);
   for (int s = 0; s < nst; ++s) {
     if (s + 1 < nst) {
-      issue(s + 1, sb + ((s + 1) & 1) * BUF);
+      issue(s + 1, sb + ((s + 1) & 1) * BUF, jn);
+      jn = load_idx(s + 2);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
