@@ -86,6 +86,15 @@ __global__ void __launch_bounds__(kGradWarps * 32) k_gradient(GradArgs a) {
 #pragma unroll
   for (int k = 0; k < V2; ++k) acc[k] = make_double2(0.0, 0.0);
   // two ratings per sub-group per trip: both gathers are in flight together
+  // indices and values of the next trip are loaded one trip ahead
+  int jn[2];
+  double rn[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int t = sg + u * R;
+    jn[u] = t < len ? a.idx[beg + t] : 0;
+    rn[u] = t < len ? a.val[beg + t] : 0.0;
+  }
   for (int t0 = 0; t0 < len; t0 += 2 * R) {
     int j[2];
     double r[2];
@@ -94,8 +103,11 @@ __global__ void __launch_bounds__(kGradWarps * 32) k_gradient(GradArgs a) {
     for (int u = 0; u < 2; ++u) {
       const int t = t0 + sg + u * R;
       ok[u] = t < len;
-      j[u] = ok[u] ? a.idx[beg + t] : 0;
-      r[u] = ok[u] ? a.val[beg + t] : 0.0;
+      j[u] = jn[u];
+      r[u] = rn[u];
+      const int tn = t + 2 * R;
+      jn[u] = tn < len ? a.idx[beg + tn] : 0;
+      rn[u] = tn < len ? a.val[beg + tn] : 0.0;
     }
     double2 m[2][V2];
 #pragma unroll
@@ -240,6 +252,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_quartic(QuartArgs a) {
     double2 xu[V2], pu[V2];
     load_row<TPR, V2>(a.x + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, xu);
     if constexpr (QUART) load_row<TPR, V2>(a.p + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, pu);
+    // index and value of the next rating are loaded one trip ahead, so a
+    // trip's row gathers never wait on their own index load
+    int jn = t < tend ? a.uidx[t] : 0;
+    double rn = t < tend ? a.uval[t] : 0.0;
     for (int64_t s = 0; s < chunk; ++s, ++t) {
       const bool ok = t < tend;
       if (ok && t >= uend) {
@@ -250,8 +266,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_quartic(QuartArgs a) {
         load_row<TPR, V2>(a.x + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, xu);
         if constexpr (QUART) load_row<TPR, V2>(a.p + static_cast<int64_t>(a.urow0 + u) * ld, ld, sl, pu);
       }
-      const int j = ok ? a.uidx[t] : 0;
-      const double r = ok ? a.uval[t] : 0.0;
+      const int j = jn;
+      const double r = rn;
+      jn = t + 1 < tend ? a.uidx[t + 1] : 0;
+      rn = t + 1 < tend ? a.uval[t + 1] : 0.0;
       const int64_t mrow = static_cast<int64_t>(a.n_u + j) * ld;
       double2 xm[V2];
       load_row<TPR, V2>(a.x + mrow, ld, sl, xm);
