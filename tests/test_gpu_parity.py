@@ -128,7 +128,7 @@ def _col_rel_err(a, b, n_f):
     return float(np.max(err[nz] / nb[nz])) if nz.any() else 0.0
 
 
-HS_RANKS = [1, 2, 3, 5, 7, 10, 15, 25, 30, 31, 50, 64, 100, 110, 127, 136, 150, 160, 180, 200]
+HS_RANKS = [1, 2, 3, 5, 7, 10, 15, 25, 30, 31, 50, 64, 75, 85, 100, 110, 127, 136, 150, 160, 180, 200]
 
 
 @pytest.mark.parametrize("n_f", HS_RANKS)
