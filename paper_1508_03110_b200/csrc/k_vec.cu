@@ -263,31 +263,95 @@ void launch_routing_count(DevRatings& R, int n_blocks, unsigned long long* d_out
 // the mt19937_64 stream of std::mt19937_64(seed) (state seeded on the host),
 // items first then users, u = (draw >> 11) * 2^-53 * (1/sqrt(n_f)) -- the
 // same operations as the host Rng::uniform, so x0 is bitwise the reference's.
-// One CTA walks the sequential twist chain (ping-pong state, two barriers
-// per 312-draw block); the draws land straight in the padded flat vector.
+//
+// The draw stream is cut into chunks of kMtChunk = 312*256 draws, one CTA per
+// chunk walking the sequential twist chain (ping-pong state, two barriers per
+// 312-draw block).  The state at each chunk start comes from jump-ahead: with
+// T the one-step transition of the 19937-bit state, T^J s = g_J(T) s for
+// g_J(x) = x^J mod phi(x) (phi the characteristic polynomial), and g(T) s is
+// the XOR, over the set coefficients i of g, of the state window at word i of
+// the sequence continuing s.  mt_jump_table.inc (tools/gen_mt_jump.py, which
+// also checks each polynomial against stepping the generator) holds g_J for
+// J = 1, 8, 64, 512 chunks; chunk states are filled level by level (at most 7
+// dependent jumps per level), every jump of a step in its own CTA.
 namespace {
 constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull, kMtUpper = 0xFFFFFFFF80000000ull,
                    kMtLower = 0x000000007FFFFFFFull;
+constexpr int kMtDeg = 19937;
+constexpr int kMtChunkTwists = 256;
+constexpr int64_t kMtChunk = 312 * static_cast<int64_t>(kMtChunkTwists);  // draws per chunk
+constexpr int kMtSeqWords = 128 * 156 + 312;  // >= kMtDeg + 312 words of the continued sequence
+constexpr int kJumpParts = 3, kJumpThreads = kJumpParts * 320;
+
+__device__ const uint64_t g_mt_jump[4][312] = {
+#include "mt_jump_table.inc"
+};
 
 __device__ __forceinline__ uint64_t mt_twist(uint64_t cur, uint64_t next, uint64_t far) {
   const uint64_t y = (cur & kMtUpper) | (next & kMtLower);
   return far ^ (y >> 1) ^ ((y & 1ull) ? kMtA : 0ull);
 }
 
-__global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restrict__ state0,
+// states[dst] = g(T) states[src], src = src0 + blockIdx.x * src_stride, dst = src + dst_off.
+__global__ void __launch_bounds__(kJumpThreads) k_mt_jump(uint64_t* __restrict__ states, int n_chunks,
+                                                           int src0, int src_stride, int dst_off,
+                                                           int poly) {
+  extern __shared__ uint64_t jw[];  // [kMtSeqWords] sequence + [kJumpParts][312] partial windows
+  const int src = src0 + static_cast<int>(blockIdx.x) * src_stride, dst = src + dst_off;
+  if (dst >= n_chunks) return;
+  const int tid = threadIdx.x;
+  if (tid < 312) jw[tid] = states[static_cast<int64_t>(src) * 312 + tid];
+  __syncthreads();
+  // continue the word sequence: 156 new words per step (w[k+312] needs w[k], w[k+1], w[k+156])
+  for (int base = 0; base + 312 < kMtSeqWords; base += 156) {
+    if (tid < 156) jw[base + 312 + tid] = mt_twist(jw[base + tid], jw[base + tid + 1], jw[base + tid + 156]);
+    __syncthreads();
+  }
+  // window k of the result: XOR of w[i + k] over the set coefficients i; the
+  // coefficient words are split over kJumpParts thread groups
+  const int part = tid / 320, k = tid % 320;
+  constexpr int WPP = 312 / kJumpParts;
+  uint64_t r = 0;
+  if (k < 312) {
+    for (int wi = part * WPP; wi < (part + 1) * WPP; ++wi) {
+      uint64_t bits = g_mt_jump[poly][wi];
+      const uint64_t* w = jw + 64 * wi + k;
+      while (bits) {
+        const int b = __ffsll(static_cast<long long>(bits)) - 1;
+        bits &= bits - 1;
+        r ^= w[b];
+      }
+    }
+    jw[kMtSeqWords + part * 312 + k] = r;
+  }
+  __syncthreads();
+  if (tid < 312) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int q = 0; q < kJumpParts; ++q) v ^= jw[kMtSeqWords + q * 312 + tid];
+    states[static_cast<int64_t>(dst) * 312 + tid] = v;
+  }
+}
+
+// One CTA per chunk: draws [chunk * kMtChunk, min(n_draws, (chunk + 1) * kMtChunk)).
+__global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restrict__ states,
                                                           int64_t n_item_draws, int64_t n_draws,
                                                           int n_f, int ld, int n_u, double scale,
                                                           double* __restrict__ x) {
   __shared__ uint64_t S[2][312];  // ping-pong state: two barriers per 312 draws
   const int tid = threadIdx.x;
-  if (tid < 312) S[0][tid] = state0[tid];
+  if (tid < 312) S[0][tid] = states[static_cast<int64_t>(blockIdx.x) * 312 + tid];
   __syncthreads();
   int cur = 0;
-  // draw k = base + tid -> (q, col) = divmod(k, n_f), kept incrementally (no
-  // 64-bit division in the chain): q < n_m are item rows, the rest user rows
-  int q = tid / n_f, col = tid % n_f;
+  const int64_t base0 = static_cast<int64_t>(blockIdx.x) * kMtChunk;
+  const int64_t end = min(n_draws, base0 + kMtChunk);
+  // draw k = base + tid -> (q, col) = divmod(k, n_f), kept incrementally (one
+  // 64-bit division per CTA): q < n_m are item rows, the rest user rows
+  int64_t q = (base0 + tid) / n_f;
+  int col = static_cast<int>((base0 + tid) % n_f);
   const int dq = 312 / n_f, dc = 312 % n_f;
-  for (int64_t base = 0; base < n_draws; base += 312) {
+  const int64_t n_m = n_item_draws / n_f;
+  for (int64_t base = base0; base < end; base += 312) {
     const int nx = cur ^ 1;
     if (tid < 156) S[nx][tid] = mt_twist(S[cur][tid], S[cur][tid + 1], S[cur][tid + 156]);
     __syncthreads();
@@ -296,7 +360,7 @@ __global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restri
     __syncthreads();
     cur = nx;
     const int64_t k = base + tid;
-    if (tid < 312 && k < n_draws) {
+    if (tid < 312 && k < end) {
       uint64_t z = S[cur][tid];
       z ^= (z >> 29) & 0x5555555555555555ull;
       z ^= (z << 17) & 0x71D67FFFEDA60000ull;
@@ -304,7 +368,7 @@ __global__ void __launch_bounds__(320) k_mt_random_init(const uint64_t* __restri
       z ^= z >> 43;
       const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
       const double val = __dmul_rn(u, scale);
-      const int64_t row = k < n_item_draws ? n_u + q : q - (n_item_draws / n_f);
+      const int64_t row = k < n_item_draws ? n_u + q : q - n_m;
       x[row * ld + col] = val;
     }
     q += dq;
@@ -322,17 +386,37 @@ void launch_random_init(Ctx* ctx, int n_f, int n_u, int n_m, uint64_t seed, doub
   uint64_t st[312];
   st[0] = seed;
   for (int i = 1; i < 312; ++i) st[i] = 6364136223846793005ull * (st[i - 1] ^ (st[i - 1] >> 62)) + i;
-  uint64_t* d = static_cast<uint64_t*>(ctx->scratch(7, sizeof st));
-  AB2_CUDA(cudaMemcpyAsync(d, st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t nm = static_cast<int64_t>(n_f) * n_m, nu = static_cast<int64_t>(n_f) * n_u;
+  const int64_t n_draws = nm + nu;
+  const int n_chunks = static_cast<int>(std::max<int64_t>(1, (n_draws + kMtChunk - 1) / kMtChunk));
+  uint64_t* states = static_cast<uint64_t*>(ctx->scratch(7, sizeof(uint64_t) * 312 * static_cast<size_t>(n_chunks)));
+  AB2_CUDA(cudaMemcpyAsync(states, st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
   const int ld = row_stride(n_f);
   AB2_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (static_cast<size_t>(n_u) + n_m) * ld, ctx->stream));
-  const int64_t nm = static_cast<int64_t>(n_f) * n_m, nu = static_cast<int64_t>(n_f) * n_u;
+  if (n_chunks > 1) {
+    // chunk states by jump-ahead: strides 512, 64, 8, 1 chunks (polynomials 3..0)
+    const size_t smem = sizeof(uint64_t) * (kMtSeqWords + kJumpParts * 312);
+    ctx->prepare_kernel(reinterpret_cast<const void*>(k_mt_jump), static_cast<int>(smem), 0, 0);
+    const int tok = ctx->begin_launch("random_init_jump");
+    for (int a = 1; a * 512 < n_chunks; ++a)
+      k_mt_jump<<<1, kJumpThreads, smem, ctx->stream>>>(states, n_chunks, (a - 1) * 512, 0, 512, 3);
+    const int strides[4] = {512, 64, 8, 1};
+    for (int lvl = 1; lvl < 4; ++lvl) {
+      const int big = strides[lvl - 1], small = strides[lvl];
+      if (small >= n_chunks) continue;
+      const int n_src = (n_chunks + big - 1) / big;
+      for (int step = 1; step < 8; ++step)
+        k_mt_jump<<<n_src, kJumpThreads, smem, ctx->stream>>>(states, n_chunks, (step - 1) * small, big,
+                                                                small, 3 - lvl);
+    }
+    ctx->end_launch(tok);
+  }
   const int t = ctx->begin_launch("random_init");
-  k_mt_random_init<<<1, 320, 0, ctx->stream>>>(d, nm, nm + nu, n_f, ld, n_u,
-                                               1.0 / std::sqrt(static_cast<double>(n_f)), x);
+  k_mt_random_init<<<n_chunks, 320, 0, ctx->stream>>>(states, nm, n_draws, n_f, ld, n_u,
+                                                     1.0 / std::sqrt(static_cast<double>(n_f)), x);
   ctx->end_launch(t);
   // (no sync: a copy from pageable memory returns once `st` has been staged,
-  // so the host goes on to build the work plans while the chain runs)
+  // so the host goes on to build the work plans while the kernels run)
 }
 
 }  // namespace ab2

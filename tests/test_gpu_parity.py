@@ -328,3 +328,22 @@ def test_device_random_init_is_the_host_stream(n_f, seed):
     s.close()
     want = P.random_init(n_f, T.n_u, T.n_m, seed)
     assert np.array_equal(np.asarray(m), np.concatenate([want.user_data, want.item_data]))
+
+
+@pytest.mark.parametrize("n_f,n_u,n_m,seed", [(100, 20000, 300, 3),       # 26 chunks: jumps of 1 and 8 chunks
+                                              (64, 100000, 2000, 0),      # 84 chunks: adds the 64-chunk jump
+                                              (100, 450000, 1000, 77)])   # 565 chunks: adds the 512-chunk jump
+def test_device_random_init_jump_ahead_is_the_host_stream(n_f, n_u, n_m, seed):
+    # x0 is generated in chunks of 312*256 draws whose start states come from
+    # mt19937_64 jump-ahead (k_vec.cu, tools/gen_mt_jump.py): still bitwise the
+    # host stream, across every jump level
+    users = np.arange(n_u, dtype=np.int32)
+    items = (users % n_m).astype(np.int32)
+    values = np.full(n_u, 3.0)
+    R = P.RatingsMatrix.from_triples(n_u, n_m, users=users, items=items, values=values)
+    cfg = P.SolverConfig(lambda_=0.1, n_f=n_f, max_iters=0, tol=0.0, seed=seed)
+    s = P.ncg.Solver(R, cfg)
+    m = s.model()
+    s.close()
+    want = P.random_init(n_f, n_u, n_m, seed)
+    assert np.array_equal(np.asarray(m), np.concatenate([want.user_data, want.item_data]))

@@ -197,3 +197,20 @@ def test_threaded_generator_bitwise_vs_sequential_oracle():
         b = P.synth.generate_triples(n_u, n_m, nnz, seed)
         for x, y in zip(a, b):
             assert x.tobytes() == y.tobytes()
+
+
+def test_mt_jump_table_jumps_the_generator():
+    # csrc/mt_jump_table.inc (tools/gen_mt_jump.py): g(T) s for the first two
+    # polynomials equals stepping std::mt19937_64 by 312*256 and 8*312*256
+    # draws; the other two are the 8th powers of their predecessors mod phi
+    # (checked when the table is generated).
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gen_mt_jump", os.path.join(root, "tools", "gen_mt_jump.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    polys = g.read_table(os.path.join(root, "paper_1508_03110_b200", "csrc", "mt_jump_table.inc"))
+    s0 = g.seed_state(20260101)
+    ref = g.words(s0, g.JUMPS[1] + g.N)
+    for p in (0, 1):
+        assert g.same_state(g.jump(s0, polys[p]), ref[g.JUMPS[p]:g.JUMPS[p] + g.N])
