@@ -1268,7 +1268,7 @@ struct Mode {
   static constexpr int GW = NB <= 4 ? 1 : (NB <= 16 ? 4 : (NB <= 20 ? 8 : 16));
 };
 
-constexpr size_t kGramBudget = size_t(3) << 30;  // bytes of partial Grams per batch
+constexpr size_t kGramBudget = size_t(8) << 30;  // bytes of partial Grams per batch
 
 // Largest block count solved by k_hs_solve_1w (one warp per column); above it
 // the warp-specialised team kernel.  ALSNCG_SOLVE_1W_MAX overrides (development A/B).
