@@ -342,9 +342,9 @@ DevRatings::~DevRatings() {
   free_view(ctx, users);
   free_view(ctx, items);
   for (auto& m : plans)
-    for (auto& kv : m) cudaFree(kv.second->block);
+    for (auto& kv : m) ctx->release(kv.second->block);
   for (auto& m : hs_plans)
-    for (auto& kv : m) cudaFree(kv.second->block);
+    for (auto& kv : m) ctx->release(kv.second->block);
 }
 
 const SegPlan& DevRatings::plan(int kind, int S) {
@@ -404,8 +404,8 @@ const SegPlan& DevRatings::plan(int kind, int S) {
   P->n_slots = n_slots;
   const size_t ns = std::max<size_t>(row.size(), 1), nm = std::max<size_t>(mrow.size(), 1);
   const size_t bytes = ns * (8 + 4 + 4 + 4) + nm * 12 + 64;
-  char* blk = nullptr;
-  AB2_CUDA(cudaMalloc(&blk, bytes));
+  // stream-ordered pool memory: no device-wide synchronisation on alloc / free
+  char* blk = static_cast<char*>(ctx->alloc(bytes));
   P->block = blk;
   P->seg_beg = reinterpret_cast<int64_t*>(blk);
   P->seg_row = reinterpret_cast<int*>(blk + ns * 8);
@@ -502,9 +502,8 @@ const HsPlan& DevRatings::hs_plan(int kind, int S, int64_t max_slots) {
     P->batches.push_back(b);
   }
   const size_t ns = std::max<size_t>(srow.size(), 1), nr = std::max<size_t>(v.nrows, 1);
-  char* blk = nullptr;
   const size_t nm = std::max<size_t>(multi.size(), 1);
-  AB2_CUDA(cudaMalloc(&blk, ns * (8 + 4 + 4 + 4) + nr * 8 + nm * 4 + 64));
+  char* blk = static_cast<char*>(ctx->alloc(ns * (8 + 4 + 4 + 4) + nr * 8 + nm * 4 + 64));
   P->block = blk;
   P->seg_beg = reinterpret_cast<int64_t*>(blk);
   P->seg_row = reinterpret_cast<int*>(blk + ns * 8);
