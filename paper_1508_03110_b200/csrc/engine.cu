@@ -174,6 +174,9 @@ L2Window::L2Window(Ctx* c, const void* base, size_t bytes) : ctx(c) {
   }
   const int max_persist = c->l2_max_persist, max_window = c->l2_max_window;
   if (max_persist <= 0 || max_window <= 0 || bytes == 0) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c->stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+    return;  // stream attributes and the persisting-L2 reset are not graph operations
   cudaStreamAttrValue v = {};
   v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
   v.accessPolicyWindow.num_bytes = std::min(bytes, static_cast<size_t>(max_window));

@@ -93,6 +93,7 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
     gbar_ = p_ = px_ = xn_ = gn_ = gbn_ = pn_ = pxn_ = nullptr;
   }
   AB2_CUDA(cudaMemsetAsync(ctx_->d_counters + kCounterFallback, 0, sizeof(unsigned), ctx_->stream));
+  use_graphs_ = std::getenv("ALSNCG_GRAPH") != nullptr;
   mark("malloc");
 
   // x0 = flatten(random_init(seed)) (ncg.cpp:154-155), generated on the
@@ -130,7 +131,49 @@ Solver::Solver(DevRatings* R, const alsncg_config& cfg, bool ncg, alsncg_snapsho
   }
 }
 
+// ncg.cpp:253-257 on the device: gradient at x_{k+1}, P(x_{k+1}), and the
+// fused pass (gbar_next, beta parts, ||g_next||^2, g_next.(-gbar_next)).  No
+// host decision falls inside this sequence, so with ALSNCG_GRAPH=1 it is
+// captured once per rotation of its buffers and replayed as a CUDA graph --
+// for launch-bound sizes (config 0: ~20 launches of a few microseconds each).
+// Capture starts at the third iteration, when every plan, scratch buffer and
+// kernel attribute the sequence needs already exists (nothing may allocate or
+// synchronise while the stream is capturing).
+void Solver::gradient_als_gbar() {
+  auto run = [&]() {
+    gradient(xn_, gn_);
+    apply_als(xn_, pxn_);
+    launch_vec(ctx_, kGbarFused, N_, xn_, pxn_, gn_, g_, 0.0, gbn_, kSlotGbar);
+  };
+  if (!use_graphs_ || ctx_->world > 1 || ctx_->profiling || k_ < 2) return run();
+  const std::array<const void*, 5> key = {xn_, gn_, pxn_, g_, gbn_};
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
+    const long before = ctx_->launches;
+    cudaGraph_t graph = nullptr;
+    AB2_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeRelaxed));
+    try {
+      run();
+    } catch (...) {
+      cudaStreamEndCapture(ctx_->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    AB2_CUDA(cudaStreamEndCapture(ctx_->stream, &graph));
+    IterGraph g;
+    g.launches = ctx_->launches - before;
+    ctx_->launches = before;
+    AB2_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    it = graphs_.emplace(key, g).first;
+  }
+  AB2_CUDA(cudaGraphLaunch(it->second.exec, ctx_->stream));
+  ctx_->launches += it->second.launches;
+}
+
 Solver::~Solver() {
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (buf_) {
     cudaSetDevice(ctx_->device);
     ctx_->release(buf_);  // stream-ordered: back to the pool after the last use
@@ -283,14 +326,12 @@ void Solver::ncg_iteration() {
       AB2_CUDA(cudaStreamWaitEvent(ctx_->stream, ctx_->ev_join, 0));
       ctx_->side_join = false;
     }
+    launch_vec(ctx_, kGbarFused, N_, xn_, pxn_, gn_, g_, 0.0, gbn_, kSlotGbar);
   } else {
-    gradient(xn_, gn_);
-    apply_als(xn_, pxn_);
+    gradient_als_gbar();
   }
   step_columns_ += gradient_columns_;
   step_columns_ += sweep_columns_;
-  // gbar_next, beta parts, ||g_next||^2 and g_next.(-gbar_next) in one pass
-  launch_vec(ctx_, kGbarFused, N_, xn_, pxn_, gn_, g_, 0.0, gbn_, kSlotGbar);
   ctx_->fetch_scalars(kSlotGbar + 4);
   const double num = ctx_->h_scalars[kSlotGbar];
   const double den_next = ctx_->h_scalars[kSlotGbar + 1];

@@ -3,7 +3,9 @@
 // branch; only scalars cross PCIe per iteration.
 #pragma once
 
+#include <array>
 #include <chrono>
+#include <map>
 #include <vector>
 
 #include "engine.h"
@@ -77,6 +79,15 @@ class Solver {
   double den_ = 0.0;    // gbar.g for the current pair (beta denominator)
   bool p_is_neg_gbar_ = true;
   bool restart_pending_ = false;
+  // CUDA graphs of the launch sequence between two host decisions (gradient,
+  // P(x), fused gbar pass), one per rotation of the buffers it touches.
+  struct IterGraph {
+    cudaGraphExec_t exec = nullptr;
+    long launches = 0;
+  };
+  std::map<std::array<const void*, 5>, IterGraph> graphs_;
+  bool use_graphs_ = false;
+  void gradient_als_gbar();
   int restarts_ = 0, fallback_steps_ = 0;
   int64_t sweep_columns_ = 0, gradient_columns_ = 0, quartic_columns_ = 0, step_columns_ = 0;
   Watch watch_;

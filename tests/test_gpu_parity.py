@@ -347,3 +347,26 @@ def test_device_random_init_jump_ahead_is_the_host_stream(n_f, n_u, n_m, seed):
     s.close()
     want = P.random_init(n_f, n_u, n_m, seed)
     assert np.array_equal(np.asarray(m), np.concatenate([want.user_data, want.item_data]))
+
+
+def test_cuda_graph_replay_is_bitwise_the_plain_iteration(monkeypatch):
+    # ALSNCG_GRAPH=1 replays gradient + P(x) + the fused gbar pass as a CUDA
+    # graph (solver.cpp gradient_als_gbar): same kernels, same arguments, so
+    # the trace and the model must be identical bit for bit
+    T = random_ratings(60, 24, 0.35, 5)
+    R, _ = both(T)
+    out = []
+    for on in (False, True):
+        if on:
+            monkeypatch.setenv("ALSNCG_GRAPH", "1")
+        else:
+            monkeypatch.delenv("ALSNCG_GRAPH", raising=False)
+        cfg = P.SolverConfig(lambda_=0.05, n_f=6, max_iters=25, tol=0.0, seed=3)
+        res = P.ncg.als_ncg_solve(R, cfg)
+        out.append(res)
+    a, b = out
+    assert a.iterations == b.iterations == 25
+    for ra, rb in zip(a.trace.records, b.trace.records):
+        assert (ra.loss, ra.grad_norm, ra.backtracks, ra.restarted) == (rb.loss, rb.grad_norm, rb.backtracks, rb.restarted)
+    assert np.array_equal(a.model.user_data, b.model.user_data)
+    assert np.array_equal(a.model.item_data, b.model.item_data)
