@@ -637,8 +637,8 @@ __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (4 * ((r 
 
 // ---------------------------------------------------------------------------
 // K3 v2 (k_hs_solve_ws): warp-specialised persistent solve.  One CTA per SM,
-// TEAMS teams of 1 + DW warps (DW = 3 for n_f <= 120; 6 or 9 DMMA warps when
-// only two or one column fit per SM), one column in flight per team (the team's
+// TEAMS teams of 1 + DW warps (DW = 3; 6 or 9 DMMA warps when only one column
+// fits per SM), one column in flight per team (the team's
 // shared block store holds that column's lower-triangular augmented Gram).
 // The measured constraint (profiles/fp64_latency.txt): DFMA and DMMA share the
 // FP64 datapath of an SM sub-partition (SMSP), and a dependent scalar FP64
@@ -671,14 +671,15 @@ struct WsSolve {
   static constexpr int TEAM_BYTES = TEAM_D * 8;
   static constexpr int FIT = (227 * 1024) / TEAM_BYTES;
   static constexpr int TEAMS = FIT > 6 ? 6 : (FIT < 1 ? 1 : FIT);
-  // Large ranks fit one or two columns per SM: their teams get more DMMA
-  // warps (WPS per SMSP 1-3).  The CTA has TEAMS * WPS warps on every SMSP; on
+  // Ranks that fit a single column per SM get more DMMA warps per team (WPS
+  // per SMSP 1-3); with two columns per SM three DMMA warps per team are still
+  // (slightly) faster than six (f = 128: 21.4 vs 22.2 ms).  The CTA has TEAMS * WPS warps on every SMSP; on
   // SMSP 0 only one per team works (the pivot warp), the others exit after
   // the prologue.  Measured (solve ms per iteration, config-1 matrix), DMMA
   // warps per team 3 / 6 / 9 / 12: NB = 20 78 / 50 / 55 / 58, NB = 26
   // 151 / 98 / 82 / 85 -- more warps shorten the update phases but lengthen
   // the two named barriers of every panel.
-  static constexpr int WPS = TEAMS == 1 ? (NB >= 24 ? 3 : 2) : (TEAMS == 2 ? 2 : 1);
+  static constexpr int WPS = TEAMS == 1 ? (NB >= 24 ? 3 : 2) : 1;
   static constexpr int DW = 3 * WPS;            // DMMA warps per team
   static constexpr int ACT = (1 + DW) * 32;     // working threads per team
   static constexpr int THREADS = TEAMS * WPS * 128;
