@@ -1277,7 +1277,7 @@ constexpr size_t kGramBudget = size_t(8) << 30;  // bytes of partial Grams per b
 // Largest block count solved by k_hs_solve_1w (one warp per column); above it
 // the warp-specialised team kernel.  ALSNCG_SOLVE_1W_MAX overrides (development A/B).
 #ifndef AB2_SOLVE_1W_MAX_NB
-#define AB2_SOLVE_1W_MAX_NB 10
+#define AB2_SOLVE_1W_MAX_NB 11
 #endif
 inline int solve_1w_max_nb() {
   static const int v = [] {
